@@ -1,0 +1,183 @@
+"""ctypes binding of libtm_w4a16.so (include/tm_w4a16.h).  Argument marshalling only.
+
+Every function here forwards torch CUDA tensors as raw device pointers plus the
+current CUDA stream to the C ABI; all computation happens in the library's
+kernels.  The library is loaded on first use; if it is missing or cannot be
+loaded the call raises (there is no CPU or PyTorch fallback).
+"""
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtm_w4a16.so")
+
+TM_LAYOUT_V1 = 1
+
+_lib = None
+
+
+class TMError(RuntimeError):
+    pass
+
+
+class tm_packed_w4(ctypes.Structure):
+    _fields_ = [
+        ("data", ctypes.c_void_p),
+        ("bytes", ctypes.c_int64),
+        ("K", ctypes.c_int32),
+        ("N", ctypes.c_int32),
+        ("group", ctypes.c_int32),
+        ("layout", ctypes.c_uint32),
+    ]
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_SIGS = {
+    "tm_pack_w4_bytes": (ctypes.c_int64, [_I, _I, _I]),
+    "tm_pack_w4": (_I, [_P, _P, _P, _I, _I, _I, ctypes.POINTER(tm_packed_w4), _P]),
+    "tm_gemm_w4a16": (_I, [_P, ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _I, _I, _P]),
+    "tm_gemm_w4a16_f16": (_I, [_P, ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _I, _I, _P]),
+    "tm_gemm_w4a16_partial_f32": (_I, [_P, ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _I, _I, _P]),
+    "tm_tp_finalize": (_I, [_P, _P, ctypes.c_int64, _P]),
+    "tm_unpack_w4": (_I, [ctypes.POINTER(tm_packed_w4), _P, _P]),
+    "tm_dequant_w4": (_I, [ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _P]),
+    "tm_set_gemm_override": (_I, [_I, _I]),
+    "tm_query_gemm_config": (_I, [_I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I)]),
+    "tm_status_string": (ctypes.c_char_p, [_I]),
+    "tm_version": (ctypes.c_char_p, []),
+}
+
+
+def lib():
+    """Load (once) and return the ctypes handle; raises if the library is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise TMError(f"{LIB_PATH} not built: run `python -m paper_2508_15601_b200.build` "
+                          "(no fallback path exists)")
+        handle = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def _check(status):
+    if status != 0:
+        raise TMError(lib().tm_status_string(status).decode())
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.is_contiguous()):
+            raise TMError("expected contiguous CUDA tensors")
+
+
+class PackedW4:
+    """A packed weight: device buffer (torch uint8 tensor) + the C descriptor."""
+
+    def __init__(self, data, K, N, group):
+        self.data = data
+        self.desc = tm_packed_w4(data.data_ptr(), data.numel(), 0, 0, 0, 0)
+        self.K, self.N, self.group = K, N, group
+
+    @property
+    def nbytes(self):
+        return self.data.numel()
+
+
+def pack_w4_bytes(K, N, group):
+    r = lib().tm_pack_w4_bytes(K, N, group)
+    if r < 0:
+        _check(int(r))
+    return int(r)
+
+
+def pack_w4(q, scales, zeros, group, stream=None, out=None):
+    """tm_pack_w4: q uint8 [K][N], scales/zeros fp16 [K/group][N] -> PackedW4."""
+    _require_cuda(q, scales, zeros)
+    K, N = q.shape
+    nbytes = pack_w4_bytes(K, N, group)
+    data = out if out is not None else torch.empty(nbytes, dtype=torch.uint8, device=q.device)
+    p = PackedW4(data, K, N, group)
+    _check(lib().tm_pack_w4(_ptr(q), _ptr(scales), _ptr(zeros), K, N, group, ctypes.byref(p.desc), _stream(stream)))
+    return p
+
+
+def _gemm(fn, A, packed, scales, zeros, out, out_dtype, stream):
+    _require_cuda(A, scales, zeros)
+    M, K = A.shape
+    N = packed.N
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype, device=A.device)
+    _require_cuda(out)
+    _check(fn(_ptr(A), ctypes.byref(packed.desc), _ptr(scales), _ptr(zeros), _ptr(out), M, N, K, _stream(stream)))
+    return out
+
+
+def gemm_w4a16(A, packed, scales, zeros, out=None, stream=None):
+    """tm_gemm_w4a16: bf16 A [M][K] x packed W -> bf16 C [M][N]."""
+    return _gemm(lib().tm_gemm_w4a16, A, packed, scales, zeros, out, torch.bfloat16, stream)
+
+
+def gemm_w4a16_f16(A, packed, scales, zeros, out=None, stream=None):
+    """tm_gemm_w4a16_f16: fp16 A -> fp16 C."""
+    return _gemm(lib().tm_gemm_w4a16_f16, A, packed, scales, zeros, out, torch.float16, stream)
+
+
+def gemm_w4a16_partial_f32(A, packed, scales, zeros, out=None, stream=None):
+    """tm_gemm_w4a16_partial_f32: bf16 A -> fp32 partial C (row-parallel TP)."""
+    return _gemm(lib().tm_gemm_w4a16_partial_f32, A, packed, scales, zeros, out, torch.float32, stream)
+
+
+def tp_finalize(x_f32, out=None, stream=None):
+    """tm_tp_finalize: fp32 -> bf16 (RNE)."""
+    _require_cuda(x_f32)
+    if out is None:
+        out = torch.empty(x_f32.shape, dtype=torch.bfloat16, device=x_f32.device)
+    _check(lib().tm_tp_finalize(_ptr(x_f32), _ptr(out), x_f32.numel(), _stream(stream)))
+    return out
+
+
+def unpack_w4(packed, stream=None):
+    out = torch.empty((packed.K, packed.N), dtype=torch.uint8, device=packed.data.device)
+    _check(lib().tm_unpack_w4(ctypes.byref(packed.desc), _ptr(out), _stream(stream)))
+    return out
+
+
+def dequant_w4(packed, scales, zeros, dtype="bf16", stream=None):
+    _require_cuda(scales, zeros)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float16
+    out = torch.empty((packed.K, packed.N), dtype=tdt, device=packed.data.device)
+    _check(lib().tm_dequant_w4(ctypes.byref(packed.desc), _ptr(scales), _ptr(zeros), _ptr(out),
+                               0 if dtype == "bf16" else 1, _stream(stream)))
+    return out
+
+
+def set_gemm_override(tile_m=0, split_k=0):
+    _check(lib().tm_set_gemm_override(tile_m, split_k))
+
+
+def query_gemm_config(M, N, K):
+    t, s, g = _I(), _I(), _I()
+    _check(lib().tm_query_gemm_config(M, N, K, ctypes.byref(t), ctypes.byref(s), ctypes.byref(g)))
+    return dict(tile_m=t.value, split_k=s.value, grid_ctas=g.value)
+
+
+def version():
+    return lib().tm_version().decode()

@@ -1,0 +1,363 @@
+// api.cu -- host side of libtm_w4a16.so: the C ABI declared in include/tm_w4a16.h.
+// Validation, launch-configuration choice, TMA descriptor encoding (cached), launches.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "../../include/tm_w4a16.h"
+#include "aux_kernels.cuh"
+#include "gemm_w4a16.cuh"
+
+namespace {
+
+using namespace w4k;
+
+constexpr int kNumSMsDefault = 148;
+
+std::atomic<int> g_override_tile{0};
+std::atomic<int> g_override_split{0};
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+tm_status check_shape(int K, int N, int group) {
+  if (K <= 0 || N <= 0) return TM_ERR_INVALID_ARG;
+  if (group != 64 && group != 128) return TM_ERR_UNSUPPORTED_SHAPE;
+  if (N % 128 || K % 64 || K % group) return TM_ERR_UNSUPPORTED_SHAPE;
+  return TM_OK;
+}
+
+tm_status from_cuda(cudaError_t e) { return e == cudaSuccess ? TM_OK : TM_ERR_CUDA; }
+
+int num_sms() {
+  static int sms = [] {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return kNumSMsDefault;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      return kNumSMsDefault;
+    return v;
+  }();
+  return sms;
+}
+
+// ---------------------------------------------------------------- TMA descriptors
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+struct MapKey {
+  const void* ptr;
+  int M, K, NT, bf16;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && M == o.M && K == o.K && NT == o.NT && bf16 == o.bf16;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = reinterpret_cast<size_t>(k.ptr);
+    h ^= (static_cast<size_t>(k.M) * 0x9E3779B97F4A7C15ull) ^ (static_cast<size_t>(k.K) << 20) ^
+         (static_cast<size_t>(k.NT) << 40) ^ static_cast<size_t>(k.bf16);
+    return h;
+  }
+};
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+tm_status act_tensor_map(const void* A, int M, int K, int NT, bool bf16, CUtensorMap* out) {
+  const MapKey key{A, M, K, NT, bf16 ? 1 : 0};
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return TM_OK;
+    }
+  }
+  auto enc = get_encode();
+  if (!enc) return TM_ERR_CUDA;
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(M)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(K) * 2};
+  const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(NT)};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                   const_cast<void*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return TM_ERR_CUDA;
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    if (g_maps.size() > 4096) g_maps.clear();
+    g_maps.emplace(key, map);
+  }
+  *out = map;
+  return TM_OK;
+}
+
+// ---------------------------------------------------------------- launch configuration
+struct Config {
+  int NT;
+  int split;
+  int grid_x, grid_y;
+};
+
+Config choose_config(int M, int N, int K) {
+  Config c{};
+  int nt = 16;
+  const int ot = g_override_tile.load();
+  if (ot > 0) {
+    nt = ot;
+  } else if (M <= 16) {
+    nt = 16;
+  } else if (M <= 32) {
+    nt = 32;
+  } else if (M <= 64) {
+    nt = 64;
+  } else if (M <= 128) {
+    nt = 128;
+  } else {
+    nt = 256;
+  }
+  c.NT = nt;
+  const int n_tiles = N / 128;
+  const int m_tiles = (M + nt - 1) / nt;
+  const int KS = K / 64;
+  int split = 1;
+  const int os = g_override_split.load();
+  if (os > 0) {
+    split = os;
+  } else if (nt <= 64) {
+    // decode: fill ~2 CTAs per SM with split-K over a cluster (<= 8, portable)
+    const int tiles = n_tiles * m_tiles;
+    const int target = 2 * num_sms();
+    split = (target + tiles - 1) / tiles;
+    if (split > 8) split = 8;
+  }
+  if (split > KS) split = KS;
+  if (split < 1) split = 1;
+  c.split = split;
+  c.grid_x = n_tiles * split;
+  c.grid_y = m_tiles;
+  return c;
+}
+
+template <int NT, bool BF16, int OUT>
+tm_status launch_gemm_t(const CUtensorMap& map, const GemmArgs& args, const Config& c, cudaStream_t stream) {
+  auto kern = w4a16_gemm_kernel<NT, BF16, OUT>;
+  const int smem = GemmCfg<NT>::smem_bytes(c.split);
+  static int configured_smem = 0;  // per instantiation
+  if (smem > configured_smem) {
+    const int max_smem = GemmCfg<NT>::smem_bytes(8);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+    if (e != cudaSuccess) return TM_ERR_CUDA;
+    configured_smem = max_smem;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(c.grid_x, c.grid_y, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[2];
+  int na = 0;
+  if (c.split > 1) {
+    attrs[na].id = cudaLaunchAttributeClusterDimension;
+    attrs[na].val.clusterDim.x = c.split;
+    attrs[na].val.clusterDim.y = 1;
+    attrs[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[na].val.programmaticStreamSerializationAllowed = 1;
+  ++na;
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, args);
+  return e == cudaSuccess ? TM_OK : TM_ERR_CUDA;
+}
+
+template <bool BF16, int OUT>
+tm_status launch_gemm(const CUtensorMap& map, const GemmArgs& args, const Config& c, cudaStream_t stream) {
+  switch (c.NT) {
+    case 16: return launch_gemm_t<16, BF16, OUT>(map, args, c, stream);
+    case 32: return launch_gemm_t<32, BF16, OUT>(map, args, c, stream);
+    case 64: return launch_gemm_t<64, BF16, OUT>(map, args, c, stream);
+    case 128: return launch_gemm_t<128, BF16, OUT>(map, args, c, stream);
+    case 256: return launch_gemm_t<256, BF16, OUT>(map, args, c, stream);
+    default: return TM_ERR_INVALID_ARG;
+  }
+}
+
+tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* scales, const void* zeros, void* C,
+                      int M, int N, int K, void* stream, bool bf16, int out_kind) {
+  if (!packed || !A || !scales || !zeros || !C || !packed->data) return TM_ERR_INVALID_ARG;
+  if (M < 0) return TM_ERR_INVALID_ARG;
+  if (packed->layout != TM_LAYOUT_V1 || packed->K != K || packed->N != N) return TM_ERR_INVALID_ARG;
+  tm_status st = check_shape(K, N, packed->group);
+  if (st != TM_OK) return st;
+  if (packed->bytes < static_cast<int64_t>(K) * N / 2) return TM_ERR_INVALID_ARG;
+  if (!aligned16(A) || !aligned16(packed->data) || !aligned16(scales) || !aligned16(zeros) || !aligned16(C))
+    return TM_ERR_MISALIGNED;
+  if (M == 0) return TM_OK;
+  const Config c = choose_config(M, N, K);
+  CUtensorMap map;
+  st = act_tensor_map(A, M, K, c.NT, bf16, &map);
+  if (st != TM_OK) return st;
+  GemmArgs args;
+  args.packed = static_cast<const uint8_t*>(packed->data);
+  args.scales = static_cast<const uint16_t*>(scales);
+  args.zeros = static_cast<const uint16_t*>(zeros);
+  args.out = C;
+  args.M = M;
+  args.N = N;
+  args.K = K;
+  args.group = packed->group;
+  args.split = c.split;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (out_kind == OUT_F32) return launch_gemm<true, OUT_F32>(map, args, c, s);
+  return bf16 ? launch_gemm<true, OUT_ACT>(map, args, c, s) : launch_gemm<false, OUT_ACT>(map, args, c, s);
+}
+
+int aux_grid(long long work, int block) {
+  long long g = (work + block - 1) / block;
+  const long long cap = static_cast<long long>(num_sms()) * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t tm_pack_w4_bytes(int K, int N, int group) {
+  const tm_status st = check_shape(K, N, group);
+  if (st != TM_OK) return st;
+  return static_cast<int64_t>(K) * N / 2;
+}
+
+tm_status tm_pack_w4(const uint8_t* q, const void* scales, const void* zeros, int K, int N, int group,
+                     tm_packed_w4* packed, void* stream) {
+  if (!q || !scales || !zeros || !packed || !packed->data) return TM_ERR_INVALID_ARG;
+  tm_status st = check_shape(K, N, group);
+  if (st != TM_OK) return st;
+  if (packed->bytes < static_cast<int64_t>(K) * N / 2) return TM_ERR_INVALID_ARG;
+  if (!aligned16(q) || !aligned16(scales) || !aligned16(zeros) || !aligned16(packed->data)) return TM_ERR_MISALIGNED;
+  const long long chunks = static_cast<long long>(K) * N / 32;
+  pack_w4_kernel<<<aux_grid(chunks, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      q, static_cast<uint4*>(packed->data), K, N);
+  st = from_cuda(cudaGetLastError());
+  if (st != TM_OK) return st;
+  packed->K = K;
+  packed->N = N;
+  packed->group = group;
+  packed->layout = TM_LAYOUT_V1;
+  return TM_OK;
+}
+
+tm_status tm_unpack_w4(const tm_packed_w4* packed, uint8_t* q_out, void* stream) {
+  if (!packed || !packed->data || !q_out) return TM_ERR_INVALID_ARG;
+  if (packed->layout != TM_LAYOUT_V1) return TM_ERR_INVALID_ARG;
+  tm_status st = check_shape(packed->K, packed->N, packed->group);
+  if (st != TM_OK) return st;
+  if (!aligned16(packed->data)) return TM_ERR_MISALIGNED;
+  const long long chunks = static_cast<long long>(packed->K) * packed->N / 32;
+  unpack_w4_kernel<<<aux_grid(chunks, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint4*>(packed->data), q_out, packed->K, packed->N);
+  return from_cuda(cudaGetLastError());
+}
+
+tm_status tm_dequant_w4(const tm_packed_w4* packed, const void* scales, const void* zeros, void* W_out, int dtype,
+                        void* stream) {
+  if (!packed || !packed->data || !scales || !zeros || !W_out) return TM_ERR_INVALID_ARG;
+  if (packed->layout != TM_LAYOUT_V1 || (dtype != 0 && dtype != 1)) return TM_ERR_INVALID_ARG;
+  tm_status st = check_shape(packed->K, packed->N, packed->group);
+  if (st != TM_OK) return st;
+  if (!aligned16(packed->data) || !aligned16(scales) || !aligned16(zeros)) return TM_ERR_MISALIGNED;
+  const long long chunks = static_cast<long long>(packed->K) * packed->N / 32;
+  auto s = static_cast<cudaStream_t>(stream);
+  const auto in = static_cast<const uint4*>(packed->data);
+  const auto sc = static_cast<const uint16_t*>(scales);
+  const auto zr = static_cast<const uint16_t*>(zeros);
+  auto out = static_cast<uint16_t*>(W_out);
+  if (dtype == 0)
+    dequant_w4_kernel<true><<<aux_grid(chunks, 256), 256, 0, s>>>(in, sc, zr, out, packed->K, packed->N, packed->group);
+  else
+    dequant_w4_kernel<false><<<aux_grid(chunks, 256), 256, 0, s>>>(in, sc, zr, out, packed->K, packed->N, packed->group);
+  return from_cuda(cudaGetLastError());
+}
+
+tm_status tm_gemm_w4a16(const void* A, const tm_packed_w4* packed, const void* scales, const void* zeros, void* C,
+                        int M, int N, int K, void* stream) {
+  return gemm_common(A, packed, scales, zeros, C, M, N, K, stream, true, OUT_ACT);
+}
+
+tm_status tm_gemm_w4a16_f16(const void* A, const tm_packed_w4* packed, const void* scales, const void* zeros, void* C,
+                            int M, int N, int K, void* stream) {
+  return gemm_common(A, packed, scales, zeros, C, M, N, K, stream, false, OUT_ACT);
+}
+
+tm_status tm_gemm_w4a16_partial_f32(const void* A, const tm_packed_w4* packed, const void* scales,
+                                    const void* zeros, float* C_partial, int M, int N, int K, void* stream) {
+  return gemm_common(A, packed, scales, zeros, C_partial, M, N, K, stream, true, OUT_F32);
+}
+
+tm_status tm_tp_finalize(const float* in_f32, void* out_bf16, int64_t count, void* stream) {
+  if (!in_f32 || !out_bf16 || count < 0) return TM_ERR_INVALID_ARG;
+  if (!aligned16(in_f32) || !aligned16(out_bf16)) return TM_ERR_MISALIGNED;
+  if (count == 0) return TM_OK;
+  auto s = static_cast<cudaStream_t>(stream);
+  const long long n4 = count / 4;
+  if (n4 > 0)
+    tp_finalize_kernel<<<aux_grid(n4, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(in_f32),
+                                                          static_cast<uint2*>(out_bf16), n4);
+  const long long tail = count - n4 * 4;
+  if (tail > 0)
+    tp_finalize_tail_kernel<<<1, 32, 0, s>>>(in_f32, static_cast<__nv_bfloat16*>(out_bf16), n4 * 4, count);
+  return from_cuda(cudaGetLastError());
+}
+
+tm_status tm_set_gemm_override(int tile_m, int split_k) {
+  if (tile_m > 0 && tile_m != 16 && tile_m != 32 && tile_m != 64 && tile_m != 128 && tile_m != 256)
+    return TM_ERR_INVALID_ARG;
+  if (split_k > 8) return TM_ERR_INVALID_ARG;
+  g_override_tile.store(tile_m > 0 ? tile_m : 0);
+  g_override_split.store(split_k > 0 ? split_k : 0);
+  return TM_OK;
+}
+
+tm_status tm_query_gemm_config(int M, int N, int K, int* tile_m, int* split_k, int* grid_ctas) {
+  if (M <= 0 || N <= 0 || K <= 0 || N % 128 || K % 64) return TM_ERR_INVALID_ARG;
+  const Config c = choose_config(M, N, K);
+  if (tile_m) *tile_m = c.NT;
+  if (split_k) *split_k = c.split;
+  if (grid_ctas) *grid_ctas = c.grid_x * c.grid_y;
+  return TM_OK;
+}
+
+const char* tm_status_string(tm_status s) {
+  switch (s) {
+    case TM_OK: return "TM_OK";
+    case TM_ERR_INVALID_ARG: return "TM_ERR_INVALID_ARG";
+    case TM_ERR_UNSUPPORTED_SHAPE: return "TM_ERR_UNSUPPORTED_SHAPE";
+    case TM_ERR_MISALIGNED: return "TM_ERR_MISALIGNED";
+    case TM_ERR_CUDA: return "TM_ERR_CUDA";
+    case TM_ERR_NO_DEVICE: return "TM_ERR_NO_DEVICE";
+  }
+  return "TM_ERR_UNKNOWN";
+}
+
+const char* tm_version(void) { return "tm_w4a16 0.1 (sm_100a, LAYOUT v1)"; }
+
+}  // extern "C"

@@ -1,0 +1,207 @@
+"""GPU parity: tm_gemm_w4a16 (+ _f16, _partial_f32) against the fp64 oracle.
+
+Tolerances (north star; DESIGN.md §4 R12): relative Frobenius error <= 5e-3 and the
+per-element bound of oracle/compare.py; closed forms are bit-exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import compare
+from oracle.gemm import gemm_f64
+from oracle.quant import dequant_rounded
+from oracle.numerics import round_to
+from paper_2508_15601_b200 import api, synth
+from tests.gpu_helpers import to_dev, to_np64, bits16
+
+pytestmark = pytest.mark.gpu
+
+TILES = [(16, 1), (16, 2), (16, 4), (16, 8), (32, 3), (64, 2), (128, 1), (256, 1), (64, 1), (128, 2)]
+
+
+@pytest.fixture(autouse=True)
+def _reset_override():
+    api.set_gemm_override(0, 0)
+    yield
+    api.set_gemm_override(0, 0)
+
+
+def _run(d, act="bf16", out="act"):
+    t = to_dev(d, act)
+    p = api.pack_w4(t["q"], t["s"], t["z"], d["group"])
+    if out == "f32":
+        C = api.gemm_w4a16_partial_f32(t["A"], p, t["s"], t["z"])
+    elif act == "bf16":
+        C = api.gemm_w4a16(t["A"], p, t["s"], t["z"])
+    else:
+        C = api.gemm_w4a16_f16(t["A"], p, t["s"], t["z"])
+    torch.cuda.synchronize()
+    return C, t, p
+
+
+def _assert_parity(C, d, act="bf16", rows=None, tag=""):
+    ref = gemm_f64(d["A"], d["q"], d["s"], d["z"], d["group"], rows=rows)
+    got = to_np64(C) if rows is None else to_np64(C)[rows]
+    r = compare.check(got, ref, d["A"], d["q"], d["s"], d["z"], d["group"], act)
+    assert r["ok"], (tag, r)
+    return r
+
+
+@pytest.mark.parametrize("act", ["bf16", "fp16"])
+@pytest.mark.parametrize("kind", ["awq", "uniform"])
+def test_tiny_config(act, kind):
+    """CFG#0: M=4 N=256 K=256 group=128."""
+    gen = synth.awq_like if kind == "awq" else synth.uniform
+    d = gen(4, 256, 256, group=128, seed=1000 if kind == "awq" else 1001, act_dtype=act)
+    C, _, _ = _run(d, act)
+    if kind == "awq" or act == "fp16":
+        _assert_parity(C, d, act)
+    else:  # uniform stress: relFro only (reading R12)
+        ref = gemm_f64(d["A"], d["q"], d["s"], d["z"], 128)
+        assert compare.relfro(to_np64(C), ref) <= compare.RELFRO_TOL
+
+
+@pytest.mark.parametrize("tile,split", TILES)
+@pytest.mark.parametrize("group", [64, 128])
+def test_every_variant_ragged(tile, split, group):
+    """Every (tile_m, split-K) variant on a shape spanning several tiles with ragged M."""
+    api.set_gemm_override(tile, split)
+    for M in (1, 3, tile - 1 if tile > 1 else 1, tile + 5, 2 * tile + 1):
+        d = synth.awq_like(M, 384, 1024, group=group, seed=M * 31 + tile + split)
+        C, _, _ = _run(d)
+        _assert_parity(C, d, tag=(tile, split, M))
+
+
+@pytest.mark.parametrize("M", [1, 2, 3, 5, 7, 8, 9, 15, 16, 17, 31, 33, 63, 65, 127, 129, 255, 257])
+def test_auto_config_ragged_M(M):
+    d = synth.awq_like(M, 512, 768, group=128, seed=100 + M)
+    C, _, _ = _run(d)
+    _assert_parity(C, d, tag=M)
+
+
+@pytest.mark.parametrize("M", [1, 8, 16])
+@pytest.mark.parametrize("N,K", [(6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)])
+def test_llama3_8b_decode_full(M, N, K):
+    """CFG#1 at full size, bench launch configuration, full fp64 oracle."""
+    d = synth.awq_like(M, N, K, group=128, seed=1001)
+    C, _, _ = _run(d)
+    _assert_parity(C, d, tag=(M, N, K))
+
+
+@pytest.mark.parametrize("N,K", [(6144, 4096), (28672, 4096), (4096, 14336)])
+def test_llama3_8b_prefill_sampled_rows(N, K):
+    """CFG#2 (M=2048): sampled rows (first, last, tile boundaries, random) vs the oracle."""
+    M = 2048
+    d = synth.awq_like(M, N, K, group=128, seed=1002)
+    C, _, _ = _run(d)
+    rng = np.random.default_rng(0)
+    rows = sorted(set([0, 1, 255, 256, 257, 1023, 1024, M - 1] + rng.integers(0, M, 24).tolist()))
+    _assert_parity(C, d, rows=rows, tag=(N, K))
+
+
+@pytest.mark.parametrize("act", ["bf16", "fp16"])
+def test_zero_weights_exact(act):
+    rng = np.random.default_rng(1)
+    K, N, g = 512, 384, 128
+    z = rng.integers(0, 16, size=(K // g, N)).astype(np.float16)
+    q = np.repeat(z.astype(np.uint8), g, axis=0)
+    s = rng.uniform(0.001, 0.1, size=(K // g, N)).astype(np.float16)
+    d = dict(A=synth.round_act(rng.normal(size=(20, K)), act), q=q, s=s, z=z, group=g, act_dtype=act)
+    C, _, _ = _run(d, act)
+    assert torch.all(C == 0)
+
+
+@pytest.mark.parametrize("act", ["bf16", "fp16"])
+def test_onehot_rows_are_dequant_rows_bit_exact(act):
+    d = synth.uniform(1, 384, 512, group=128, seed=9, act_dtype=act)
+    ks = [0, 1, 63, 64, 127, 128, 300, 511]
+    A = np.zeros((len(ks), 512), dtype=np.float32)
+    for m, k in enumerate(ks):
+        A[m, k] = 1.0
+    d["A"] = A
+    C, _, _ = _run(d, act)
+    W = dequant_rounded(d["q"], d["s"], d["z"], 128, act)
+    assert np.array_equal(to_np64(C), W[ks])
+
+
+def test_ones_activation_power_of_two_scales_bit_exact():
+    rng = np.random.default_rng(12)
+    K, N, g = 1024, 256, 128
+    q = rng.integers(0, 16, size=(K, N), dtype=np.uint8)
+    z = rng.integers(0, 16, size=(K // g, N)).astype(np.float16)
+    s = np.full((K // g, N), 2.0 ** -5, dtype=np.float16)
+    d = dict(A=np.ones((3, K), dtype=np.float32), q=q, s=s, z=z, group=g, act_dtype="bf16")
+    C, _, _ = _run(d)
+    exact = gemm_f64(d["A"], q, s, z, g)
+    assert np.array_equal(to_np64(C), round_to(exact, "bf16"))
+
+
+def test_doubling_activation_doubles_output():
+    d = synth.awq_like(9, 256, 512, seed=21)
+    C1, _, _ = _run(d)
+    d2 = dict(d, A=d["A"] * 2.0)
+    C2, _, _ = _run(d2)
+    assert torch.equal(C2.float(), 2.0 * C1.float())
+
+
+def test_deterministic_run_to_run():
+    d = synth.awq_like(16, 1024, 4096, seed=33)
+    t = to_dev(d)
+    p = api.pack_w4(t["q"], t["s"], t["z"], 128)
+    outs = [bits16(api.gemm_w4a16(t["A"], p, t["s"], t["z"])) for _ in range(3)]
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+def test_partial_f32_and_finalize():
+    d = synth.awq_like(16, 512, 2048, seed=44)
+    C, t, p = _run(d, out="f32")
+    assert C.dtype == torch.float32
+    _assert_parity(C, d, act="bf16")
+    Cb = api.tp_finalize(C)
+    assert torch.equal(Cb, C.to(torch.bfloat16))
+    api.set_gemm_override(16, 1)
+    Cf = api.gemm_w4a16_partial_f32(t["A"], p, t["s"], t["z"])
+    Cbf = api.gemm_w4a16(t["A"], p, t["s"], t["z"])
+    assert torch.equal(Cf.to(torch.bfloat16), Cbf)
+
+
+def test_n_shard_concatenation_bit_exact():
+    """Column-parallel TP (§8(e)): packing column shards and running them separately gives the
+    same bits as the full GEMM when the launch configuration is held fixed."""
+    d = synth.awq_like(16, 1024, 1024, seed=55)
+    api.set_gemm_override(16, 2)
+    C, t, _ = _run(d)
+    parts = []
+    for r in range(4):
+        cols = slice(r * 256, (r + 1) * 256)
+        qs, ss, zs = (x[:, cols].contiguous() for x in (t["q"], t["s"], t["z"]))
+        ps = api.pack_w4(qs, ss, zs, 128)
+        parts.append(api.gemm_w4a16(t["A"], ps, ss, zs))
+    assert torch.equal(torch.cat(parts, dim=1), C)
+
+
+def test_k_shard_partials_sum():
+    """Row-parallel TP: sum of fp32 partials over K shards matches the oracle."""
+    d = synth.awq_like(8, 512, 4096, seed=66)
+    t = to_dev(d)
+    acc = None
+    for r in range(4):
+        ks = slice(r * 1024, (r + 1) * 1024)
+        gs = slice(r * 8, (r + 1) * 8)
+        qs, ss, zs = t["q"][ks].contiguous(), t["s"][gs].contiguous(), t["z"][gs].contiguous()
+        ps = api.pack_w4(qs, ss, zs, 128)
+        part = api.gemm_w4a16_partial_f32(t["A"][:, ks].contiguous(), ps, ss, zs)
+        acc = part if acc is None else acc + part
+    _assert_parity(api.tp_finalize(acc), d)
+
+
+def test_m_zero_is_noop_and_errors():
+    d = synth.awq_like(1, 256, 256, seed=1)
+    t = to_dev(d)
+    p = api.pack_w4(t["q"], t["s"], t["z"], 128)
+    out = torch.full((0, 256), 7, dtype=torch.bfloat16, device="cuda")
+    api.gemm_w4a16(t["A"][:0], p, t["s"], t["z"], out=out)
+    bad = api.PackedW4(p.data, 256, 256, 128)  # descriptor never filled by tm_pack_w4
+    with pytest.raises(api.TMError, match="INVALID_ARG"):
+        api.gemm_w4a16(t["A"], bad, t["s"], t["z"])
