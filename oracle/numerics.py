@@ -55,6 +55,16 @@ def round_fp16(x):
     return _rne(x, **FP16)
 
 
+def ulp(x, dtype):
+    """Spacing of `dtype` values at |x| (the binade's quantum; subnormal spacing below
+    the smallest normal).  Used for the half-ulp output-rounding allowance (reading R12)."""
+    fmt = BF16 if dtype == "bf16" else FP16
+    x = np.abs(np.asarray(x, dtype=np.float64))
+    _, E = np.frexp(x)  # frexp(0) gives E = 0, clamped to emin below (subnormal spacing)
+    e = np.maximum(np.where(x > 0, E - 1, fmt["emin"]), fmt["emin"])
+    return np.ldexp(1.0, e - (fmt["p"] - 1))
+
+
 def round_to(x, dtype):
     """dtype in {'bf16', 'fp16'}."""
     if dtype == "bf16":

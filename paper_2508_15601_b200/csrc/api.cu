@@ -113,6 +113,16 @@ struct Config {
   int grid_x, grid_y;
 };
 
+int max_split_for(int nt) {
+  switch (nt) {
+    case 16: return GemmCfg<16>::MAX_SPLIT;
+    case 32: return GemmCfg<32>::MAX_SPLIT;
+    case 64: return GemmCfg<64>::MAX_SPLIT;
+    case 128: return GemmCfg<128>::MAX_SPLIT;
+    default: return GemmCfg<256>::MAX_SPLIT;
+  }
+}
+
 Config choose_config(int M, int N, int K) {
   Config c{};
   int nt = 16;
@@ -146,6 +156,7 @@ Config choose_config(int M, int N, int K) {
     if (split > 8) split = 8;
   }
   if (split > KS) split = KS;
+  if (split > max_split_for(nt)) split = max_split_for(nt);
   if (split < 1) split = 1;
   c.split = split;
   c.grid_x = n_tiles * split;
@@ -158,10 +169,14 @@ tm_status launch_gemm_t(const CUtensorMap& map, const GemmArgs& args, const Conf
   auto kern = w4a16_gemm_kernel<NT, BF16, OUT>;
   const int smem = GemmCfg<NT>::smem_bytes(c.split);
   static int configured_smem = 0;  // per instantiation
+  if (c.split > GemmCfg<NT>::MAX_SPLIT) return TM_ERR_INVALID_ARG;
   if (smem > configured_smem) {
-    const int max_smem = GemmCfg<NT>::smem_bytes(8);
+    const int max_smem = GemmCfg<NT>::smem_bytes(GemmCfg<NT>::MAX_SPLIT);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-    if (e != cudaSuccess) return TM_ERR_CUDA;
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();  // do not leave a stale error for the next launch check
+      return TM_ERR_CUDA;
+    }
     configured_smem = max_smem;
   }
   cudaLaunchConfig_t cfg{};
@@ -184,7 +199,11 @@ tm_status launch_gemm_t(const CUtensorMap& map, const GemmArgs& args, const Conf
   cfg.attrs = attrs;
   cfg.numAttrs = na;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, args);
-  return e == cudaSuccess ? TM_OK : TM_ERR_CUDA;
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return TM_ERR_CUDA;
+  }
+  return TM_OK;
 }
 
 template <bool BF16, int OUT>
@@ -201,15 +220,16 @@ tm_status launch_gemm(const CUtensorMap& map, const GemmArgs& args, const Config
 
 tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* scales, const void* zeros, void* C,
                       int M, int N, int K, void* stream, bool bf16, int out_kind) {
-  if (!packed || !A || !scales || !zeros || !C || !packed->data) return TM_ERR_INVALID_ARG;
+  if (!packed || !scales || !zeros || !packed->data) return TM_ERR_INVALID_ARG;
   if (M < 0) return TM_ERR_INVALID_ARG;
   if (packed->layout != TM_LAYOUT_V1 || packed->K != K || packed->N != N) return TM_ERR_INVALID_ARG;
   tm_status st = check_shape(K, N, packed->group);
   if (st != TM_OK) return st;
   if (packed->bytes < static_cast<int64_t>(K) * N / 2) return TM_ERR_INVALID_ARG;
+  if (M == 0) return TM_OK;  // no-op; A and C may be empty (null) tensors
+  if (!A || !C) return TM_ERR_INVALID_ARG;
   if (!aligned16(A) || !aligned16(packed->data) || !aligned16(scales) || !aligned16(zeros) || !aligned16(C))
     return TM_ERR_MISALIGNED;
-  if (M == 0) return TM_OK;
   const Config c = choose_config(M, N, K);
   CUtensorMap map;
   st = act_tensor_map(A, M, K, c.NT, bf16, &map);
@@ -331,7 +351,7 @@ tm_status tm_tp_finalize(const float* in_f32, void* out_bf16, int64_t count, voi
 tm_status tm_set_gemm_override(int tile_m, int split_k) {
   if (tile_m > 0 && tile_m != 16 && tile_m != 32 && tile_m != 64 && tile_m != 128 && tile_m != 256)
     return TM_ERR_INVALID_ARG;
-  if (split_k > 8) return TM_ERR_INVALID_ARG;
+  if (split_k > 8 || (split_k > 0 && tile_m > 0 && split_k > max_split_for(tile_m))) return TM_ERR_INVALID_ARG;
   g_override_tile.store(tile_m > 0 ? tile_m : 0);
   g_override_split.store(split_k > 0 ? split_k : 0);
   return TM_OK;

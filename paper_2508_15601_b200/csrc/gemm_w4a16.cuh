@@ -57,6 +57,8 @@ struct GemmCfg {
   static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
   static constexpr int HDR = 1024;  // barriers + tmem pointer
   static constexpr int RING = STAGES * (ACT_BYTES + kBlobBytes + kSZBytes);
+  // largest split-K whose DSMEM reduction buffer fits next to the header (<= ~200 KB)
+  static constexpr int MAX_SPLIT = (1 + (200 * 1024) / (NT * kBN * 4)) < 8 ? (1 + (200 * 1024) / (NT * kBN * 4)) : 8;
   static int smem_bytes(int split) {
     const int red = (split - 1) * NT * kBN * 4;
     return 1024 /*align slack*/ + HDR + (RING > red ? RING : red);

@@ -55,9 +55,9 @@ def test_tiny_config(act, kind):
     gen = synth.awq_like if kind == "awq" else synth.uniform
     d = gen(4, 256, 256, group=128, seed=1000 if kind == "awq" else 1001, act_dtype=act)
     C, _, _ = _run(d, act)
-    if kind == "awq" or act == "fp16":
+    if kind == "awq":
         _assert_parity(C, d, act)
-    else:  # uniform stress: relFro only (reading R12)
+    else:  # uniform stress: relFro only (reading R12; DESIGN.md §6)
         ref = gemm_f64(d["A"], d["q"], d["s"], d["z"], 128)
         assert compare.relfro(to_np64(C), ref) <= compare.RELFRO_TOL
 
@@ -157,7 +157,7 @@ def test_partial_f32_and_finalize():
     d = synth.awq_like(16, 512, 2048, seed=44)
     C, t, p = _run(d, out="f32")
     assert C.dtype == torch.float32
-    _assert_parity(C, d, act="bf16")
+    _assert_parity(C, d, act="fp32")
     Cb = api.tp_finalize(C)
     assert torch.equal(Cb, C.to(torch.bfloat16))
     api.set_gemm_override(16, 1)

@@ -109,3 +109,21 @@ def test_compare_metrics():
     assert b_h == pytest.approx(1e-2 * 0.5) and b_bf == pytest.approx(15 * 1e-2 * 0.5)
     r = compare.check(C * (1 + 1e-3), C, A, q, s, z, 128, "fp16")
     assert r["relfro"] == pytest.approx(1e-3) and r["argmax"] == (1, 1)
+
+
+def test_compare_half_ulp_allowance():
+    """An output that is exactly the RNE of the reference passes even when the accumulated
+    bound B is tiny (reading R12: one final output rounding is allowed half an ulp)."""
+    from oracle.numerics import round_bf16
+    rng = np.random.default_rng(0)
+    C_ref = rng.normal(0, 3, size=(4, 128))
+    q = np.zeros((128, 128), dtype=np.uint8)
+    z = np.zeros((1, 128), dtype=np.float16)
+    s = np.full((1, 128), 1e-4, dtype=np.float16)
+    A = np.full((4, 128), 1e-3)
+    r = compare.check(round_bf16(C_ref), C_ref, A, q, s, z, 128, "bf16")
+    assert r["max_ratio"] <= 1.0
+    # an error of one full ulp fails
+    from oracle.numerics import ulp
+    r = compare.check(C_ref + ulp(C_ref, "bf16"), C_ref, A, q, s, z, 128, "bf16")
+    assert r["max_ratio"] > 1.0

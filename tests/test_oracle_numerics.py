@@ -73,3 +73,25 @@ def test_bits_roundtrip():
     x = np.array([0.0, -0.0, 1.0, -2.5, 65504.0, 2.0 ** -24])
     assert np.array_equal(fp16_bits(x).view(np.float16).astype(np.float64), x)
     assert fp16_bits(np.array([-0.0]))[0] == 0x8000
+
+
+def test_ulp_matches_numpy_spacing_fp16():
+    from oracle.numerics import ulp
+    x = np.array([1.0, 3.0, 32768.0, 2.0 ** -14, 2.0 ** -20, 1000.0, 0.1])
+    ref = np.abs(np.spacing(x.astype(np.float16)).astype(np.float64))
+    assert np.array_equal(ulp(x, "fp16"), ref)
+    assert ulp(0.0, "fp16") == 2.0 ** -24
+
+
+def test_ulp_bf16():
+    from oracle.numerics import ulp
+    assert ulp(1.0, "bf16") == 2.0 ** -7
+    assert ulp(3.0, "bf16") == 2.0 ** -6
+    assert ulp(-5.0, "bf16") == 2.0 ** -5
+    # the ulp is the step between consecutive bf16 values (independent bit-level check)
+    import struct
+    for v in (1.0, 3.5, 1e-3, 300.0):
+        b = struct.unpack("<I", struct.pack("<f", v))[0] >> 16
+        nxt = struct.unpack("<f", struct.pack("<I", (b + 1) << 16))[0]
+        cur = struct.unpack("<f", struct.pack("<I", b << 16))[0]
+        assert ulp(cur, "bf16") == nxt - cur
