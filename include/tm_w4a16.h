@@ -7,7 +7,8 @@
  * Conventions for every entry point
  *   - All tensor pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors)
  *     owned by the caller; the library keeps no reference after the call returns.
- *     The library allocates no device memory.
+ *     The only device memory the library allocates is the per-stream stream-K
+ *     workspace of tm_gemm_* (see below).
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *     Every call only enqueues work on `stream` and returns; the caller keeps the
  *     buffers alive until the stream has completed.
@@ -79,8 +80,10 @@ tm_status tm_pack_w4(const uint8_t* q, const void* scales, const void* zeros,
  *   packed : descriptor filled by tm_pack_w4 (packed->K == K, packed->N == N)       (in)
  *   scales, zeros : fp16 [K/group][N] (group from the descriptor)                  (in)
  *   C      : bf16 [M][N]                                                           (out)
- * M <= 64 uses a split-K variant whose fp32 partials are reduced through cluster
- * shared memory in fixed rank order: results are deterministic run to run.          */
+ * M <= 64 uses a persistent stream-K kernel (one CTA per SM, equal k-chunk ranges);
+ * tiles shared by several CTAs are reduced in fixed k order through a library-owned
+ * per-stream fp32 workspace (allocated on first use -- do that first call outside CUDA
+ * graph capture).  Results are deterministic run to run.                              */
 tm_status tm_gemm_w4a16(const void* A, const tm_packed_w4* packed,
                         const void* scales, const void* zeros, void* C,
                         int M, int N, int K, void* stream);
@@ -109,12 +112,20 @@ tm_status tm_unpack_w4(const tm_packed_w4* packed, uint8_t* q_out, void* stream)
 tm_status tm_dequant_w4(const tm_packed_w4* packed, const void* scales, const void* zeros,
                         void* W_out, int dtype, void* stream);
 
-/* Force a launch configuration (tests / benchmarking only).  split_k <= 0 and
- * tile_m <= 0 restore the automatic choice.  tile_m in {16, 32, 64, 128, 256}. */
+/* Force a launch configuration (tests / benchmarking only).  tile_m in {16,32,64,128,256}
+ * (<= 0: automatic).  split_k > 0: tiled kernel with split_k CTAs per tile along K (cluster
+ * DSMEM reduction); split_k < 0: persistent stream-K kernel with -split_k CTAs; 0: automatic
+ * (stream-K with one CTA per SM for tile_m <= 64, tiled kernel otherwise).
+ * tm_query_gemm_config reports split_k < 0 for the stream-K kernel (its CTA count).      */
 tm_status tm_set_gemm_override(int tile_m, int split_k);
 
 /* Launch configuration the next tm_gemm_* call with these sizes would use. */
 tm_status tm_query_gemm_config(int M, int N, int K, int* tile_m, int* split_k, int* grid_ctas);
+
+/* Debug timeline: when buf != NULL every GEMM CTA writes 160 uint32 events (clock cycles
+ * since CTA start; slot 0 = %globaltimer ns) at buf[cta * 160 + slot].  The buffer must
+ * hold grid_ctas * 160 * 4 bytes.  NULL disables tracing (the default).               */
+tm_status tm_set_trace(void* buf, int64_t bytes);
 
 /* Human-readable status; library version string.                                     */
 const char* tm_status_string(tm_status status);

@@ -47,6 +47,7 @@ _SIGS = {
     "tm_dequant_w4": (_I, [ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _P]),
     "tm_set_gemm_override": (_I, [_I, _I]),
     "tm_query_gemm_config": (_I, [_I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I)]),
+    "tm_set_trace": (_I, [_P, ctypes.c_int64]),
     "tm_status_string": (ctypes.c_char_p, [_I]),
     "tm_version": (ctypes.c_char_p, []),
 }
@@ -177,6 +178,14 @@ def query_gemm_config(M, N, K):
     t, s, g = _I(), _I(), _I()
     _check(lib().tm_query_gemm_config(M, N, K, ctypes.byref(t), ctypes.byref(s), ctypes.byref(g)))
     return dict(tile_m=t.value, split_k=s.value, grid_ctas=g.value)
+
+
+def set_trace(buf=None):
+    """Debug: enable (torch int32 CUDA tensor) or disable (None) the per-CTA GEMM timeline."""
+    if buf is None:
+        _check(lib().tm_set_trace(None, 0))
+    else:
+        _check(lib().tm_set_trace(_ptr(buf), buf.numel() * buf.element_size()))
 
 
 def version():

@@ -13,6 +13,7 @@
 #include "../../include/tm_w4a16.h"
 #include "aux_kernels.cuh"
 #include "gemm_w4a16.cuh"
+#include "gemm_sk.cuh"
 
 namespace {
 
@@ -22,6 +23,7 @@ constexpr int kNumSMsDefault = 148;
 
 std::atomic<int> g_override_tile{0};
 std::atomic<int> g_override_split{0};
+uint32_t* g_trace = nullptr;  // debug timeline buffer (tm_set_trace)
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -106,12 +108,119 @@ tm_status act_tensor_map(const void* A, int M, int K, int NT, bool bf16, CUtenso
   return TM_OK;
 }
 
+// 3-D activation map for the stream-K kernel: dims {64, M, K/64}, strides {2K, 128} bytes,
+// box {64, NT, CH/64}: one request lands CH/64 SW128 sub-tiles of NT x 64.
+tm_status act_tensor_map_3d(const void* A, int M, int K, int NT, int blobs, bool bf16, CUtensorMap* out) {
+  const MapKey key{A, M, K, NT | (blobs << 16) | (1 << 30), bf16 ? 1 : 0};
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return TM_OK;
+    }
+  }
+  auto enc = get_encode();
+  if (!enc) return TM_ERR_CUDA;
+  CUtensorMap map;
+  const cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(K / 64)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(K) * 2, 128};
+  const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(NT), static_cast<cuuint32_t>(blobs)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
+                   const_cast<void*>(A), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return TM_ERR_CUDA;
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    if (g_maps.size() > 4096) g_maps.clear();
+    g_maps.emplace(key, map);
+  }
+  *out = map;
+  return TM_OK;
+}
+
+// 2-D map over s or z ([K/g][N] fp16): box {128 columns, 8 groups}.
+tm_status sz_tensor_map(const void* p, int G, int N, CUtensorMap* out) {
+  const MapKey key{p, G, N, 8 | (2 << 30), 2};
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return TM_OK;
+    }
+  }
+  auto enc = get_encode();
+  if (!enc) return TM_ERR_CUDA;
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(G)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(N) * 2};
+  const cuuint32_t box[2] = {128, 8};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(p), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return TM_ERR_CUDA;
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    if (g_maps.size() > 4096) g_maps.clear();
+    g_maps.emplace(key, map);
+  }
+  *out = map;
+  return TM_OK;
+}
+
+// ---------------------------------------------------------------- stream-K workspace
+// Per-stream device buffer: [counters: 64K ints][fp32 partial slots].  Counters are zeroed once
+// at allocation and returned to zero by the kernel's last contributor of every split tile.
+struct Workspace {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+constexpr size_t kCounterBytes = 65536 * sizeof(int);
+std::mutex g_ws_mu;
+std::unordered_map<cudaStream_t, Workspace> g_ws;
+
+tm_status get_workspace(cudaStream_t stream, size_t partial_bytes, int n_counters, int** counters, float** partials) {
+  if (n_counters > 65536) return TM_ERR_UNSUPPORTED_SHAPE;
+  const size_t need = kCounterBytes + partial_bytes;
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  Workspace& w = g_ws[stream];
+  if (w.bytes < need) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      (void)cudaGetLastError();
+      return TM_ERR_CUDA;  // first use of a shape class must happen outside graph capture
+    }
+    if (w.ptr) {
+      if (cudaStreamSynchronize(stream) != cudaSuccess) return TM_ERR_CUDA;
+      cudaFree(w.ptr);
+      w.ptr = nullptr;
+      w.bytes = 0;
+    }
+    size_t alloc = need < (size_t(16) << 20) ? (size_t(16) << 20) : need;
+    if (cudaMalloc(&w.ptr, alloc) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return TM_ERR_CUDA;
+    }
+    if (cudaMemset(w.ptr, 0, kCounterBytes) != cudaSuccess) return TM_ERR_CUDA;
+    w.bytes = alloc;
+  }
+  *counters = static_cast<int*>(w.ptr);
+  *partials = reinterpret_cast<float*>(static_cast<uint8_t*>(w.ptr) + kCounterBytes);
+  return TM_OK;
+}
+
 // ---------------------------------------------------------------- launch configuration
 struct Config {
+  int kind;  // 0 = classic tiles (+ cluster split-K), 1 = persistent stream-K
   int NT;
-  int split;
+  int split;  // classic: CTAs per tile along K; stream-K: number of persistent CTAs
   int grid_x, grid_y;
 };
+
+int sk_chunk(int nt) { return nt <= 64 ? 256 : (nt <= 128 ? 128 : 64); }
 
 int max_split_for(int nt) {
   switch (nt) {
@@ -146,6 +255,19 @@ Config choose_config(int M, int N, int K) {
   const int KS = K / 64;
   int split = 1;
   const int os = g_override_split.load();
+  if (os < 0 || (os == 0 && nt <= 64)) {
+    // persistent stream-K: one CTA per SM (or -os CTAs when forced), equal chunk ranges
+    c.kind = 1;
+    const int ch = sk_chunk(nt);
+    const long long total = static_cast<long long>(m_tiles) * n_tiles * ((K + ch - 1) / ch);
+    long long P = os < 0 ? -os : num_sms();
+    if (P > total) P = total;
+    c.split = static_cast<int>(P);
+    c.grid_x = c.split;
+    c.grid_y = 1;
+    return c;
+  }
+  c.kind = 0;
   if (os > 0) {
     split = os;
   } else if (nt <= 64) {
@@ -206,6 +328,71 @@ tm_status launch_gemm_t(const CUtensorMap& map, const GemmArgs& args, const Conf
   return TM_OK;
 }
 
+template <int NT, bool BF16, int OUT>
+tm_status launch_sk_t(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream) {
+  using Cfg = SkCfg<NT>;
+  auto kern = w4a16_sk_kernel<NT, BF16, OUT>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return TM_ERR_CUDA;
+    }
+    configured = true;
+  }
+  CUtensorMap ma, ms, mz;
+  tm_status st = act_tensor_map_3d(A, g.M, g.K, NT, Cfg::BLOBS, BF16, &ma);
+  if (st != TM_OK) return st;
+  st = sz_tensor_map(g.scales, g.K / g.group, g.N, &ms);
+  if (st != TM_OK) return st;
+  st = sz_tensor_map(g.zeros, g.K / g.group, g.N, &mz);
+  if (st != TM_OK) return st;
+  SkArgs a;
+  a.packed = g.packed;
+  a.out = g.out;
+  a.M = g.M;
+  a.N = g.N;
+  a.K = g.K;
+  a.group = g.group;
+  a.n_tiles = g.N / 128;
+  a.m_tiles = (g.M + NT - 1) / NT;
+  a.kc = (g.K + Cfg::CH - 1) / Cfg::CH;
+  a.total = static_cast<long long>(a.m_tiles) * a.n_tiles * a.kc;
+  a.trace = g_trace;
+  if (a.m_tiles * a.n_tiles > 65536) return TM_ERR_UNSUPPORTED_SHAPE;
+  st = get_workspace(stream, static_cast<size_t>(2) * c.split * NT * 128 * sizeof(float), a.m_tiles * a.n_tiles,
+                     &a.counters, &a.workspace);
+  if (st != TM_OK) return st;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(c.split, 1, 1);
+  cfg.blockDim = dim3(kSkThreads, 1, 1);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, ms, mz, a);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return TM_ERR_CUDA;
+  }
+  return TM_OK;
+}
+
+template <bool BF16, int OUT>
+tm_status launch_sk(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream) {
+  switch (c.NT) {
+    case 16: return launch_sk_t<16, BF16, OUT>(A, g, c, stream);
+    case 32: return launch_sk_t<32, BF16, OUT>(A, g, c, stream);
+    case 64: return launch_sk_t<64, BF16, OUT>(A, g, c, stream);
+    case 128: return launch_sk_t<128, BF16, OUT>(A, g, c, stream);
+    case 256: return launch_sk_t<256, BF16, OUT>(A, g, c, stream);
+    default: return TM_ERR_INVALID_ARG;
+  }
+}
+
 template <bool BF16, int OUT>
 tm_status launch_gemm(const CUtensorMap& map, const GemmArgs& args, const Config& c, cudaStream_t stream) {
   switch (c.NT) {
@@ -231,9 +418,6 @@ tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* sca
   if (!aligned16(A) || !aligned16(packed->data) || !aligned16(scales) || !aligned16(zeros) || !aligned16(C))
     return TM_ERR_MISALIGNED;
   const Config c = choose_config(M, N, K);
-  CUtensorMap map;
-  st = act_tensor_map(A, M, K, c.NT, bf16, &map);
-  if (st != TM_OK) return st;
   GemmArgs args;
   args.packed = static_cast<const uint8_t*>(packed->data);
   args.scales = static_cast<const uint16_t*>(scales);
@@ -244,7 +428,15 @@ tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* sca
   args.K = K;
   args.group = packed->group;
   args.split = c.split;
+  args.trace = g_trace;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c.kind == 1) {
+    if (out_kind == OUT_F32) return launch_sk<true, OUT_F32>(A, args, c, s);
+    return bf16 ? launch_sk<true, OUT_ACT>(A, args, c, s) : launch_sk<false, OUT_ACT>(A, args, c, s);
+  }
+  CUtensorMap map;
+  st = act_tensor_map(A, M, K, c.NT, bf16, &map);
+  if (st != TM_OK) return st;
   if (out_kind == OUT_F32) return launch_gemm<true, OUT_F32>(map, args, c, s);
   return bf16 ? launch_gemm<true, OUT_ACT>(map, args, c, s) : launch_gemm<false, OUT_ACT>(map, args, c, s);
 }
@@ -352,8 +544,9 @@ tm_status tm_set_gemm_override(int tile_m, int split_k) {
   if (tile_m > 0 && tile_m != 16 && tile_m != 32 && tile_m != 64 && tile_m != 128 && tile_m != 256)
     return TM_ERR_INVALID_ARG;
   if (split_k > 8 || (split_k > 0 && tile_m > 0 && split_k > max_split_for(tile_m))) return TM_ERR_INVALID_ARG;
+  if (split_k < -4096) return TM_ERR_INVALID_ARG;
   g_override_tile.store(tile_m > 0 ? tile_m : 0);
-  g_override_split.store(split_k > 0 ? split_k : 0);
+  g_override_split.store(split_k);
   return TM_OK;
 }
 
@@ -363,6 +556,7 @@ tm_status tm_query_gemm_config(int M, int N, int K, int* tile_m, int* split_k, i
   if (tile_m) *tile_m = c.NT;
   if (split_k) *split_k = c.split;
   if (grid_ctas) *grid_ctas = c.grid_x * c.grid_y;
+  if (split_k && c.kind == 1) *split_k = -c.split;  // negative: persistent stream-K CTA count
   return TM_OK;
 }
 
@@ -376,6 +570,12 @@ const char* tm_status_string(tm_status s) {
     case TM_ERR_NO_DEVICE: return "TM_ERR_NO_DEVICE";
   }
   return "TM_ERR_UNKNOWN";
+}
+
+tm_status tm_set_trace(void* buf, int64_t bytes) {
+  if (buf && bytes < 4) return TM_ERR_INVALID_ARG;
+  g_trace = static_cast<uint32_t*>(buf);
+  return TM_OK;
 }
 
 const char* tm_version(void) { return "tm_w4a16 0.1 (sm_100a, LAYOUT v1)"; }

@@ -45,7 +45,19 @@ struct GemmArgs {
   void* out;               // [M][N] bf16/fp16 or fp32
   int M, N, K, group;
   int split;  // S: CTAs per tile along K (cluster size)
+  uint32_t* trace;  // optional per-CTA timeline (debug; nullptr in production)
 };
+
+constexpr int kTraceSlots = 160;
+// trace slot layout per CTA: 0 globaltimer(ns) at start, 1 setup done, 2 producer start,
+// 3+i producer issue of stage i, 35+i dequant full-wait done, 67+i dequant A-stage arrive,
+// 99+i MMA issue, 131 epilogue start, 132 epilogue end, 133 kernel end (clock cycles since start)
+#define TM_TRACE(slot)                                                                        \
+  do {                                                                                        \
+    if (args.trace)                                                                           \
+      args.trace[(blockIdx.y * gridDim.x + blockIdx.x) * kTraceSlots + (slot)] =               \
+          static_cast<uint32_t>(clock64() - t_start);                                         \
+  } while (0)
 
 template <int NT>
 struct GemmCfg {
@@ -96,6 +108,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
+  const long long t_start = clock64();
+  if (args.trace && threadIdx.x == 0) {
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    args.trace[(blockIdx.y * gridDim.x + blockIdx.x) * kTraceSlots] = static_cast<uint32_t>(gt);
+  }
 
   const int S = args.split;
   const int nt = blockIdx.x / S;
@@ -127,6 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
+  if (threadIdx.x == 0) TM_TRACE(1);
   const uint32_t tmem_acc = tmem_base;
   const uint32_t tmem_a0 = tmem_base + Cfg::ACC_COLS;
 
@@ -139,10 +158,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint8_t* blob_g = args.packed + (static_cast<size_t>(nt) * KS + ks0) * kBlobBytes;
       const uint64_t pol_stream = policy_evict_first();
       const bool stream_weights = gridDim.y == 1;  // weights read once: do not keep them in L2
+      TM_TRACE(2);
       for (int i = 0; i < nks; ++i) {
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
         mbar_wait(bar_empty + 8 * s, ph ^ 1);
+        if (i < 32) TM_TRACE(3 + i);
         const int ks = ks0 + i;
         const int g = (ks * kBK) / args.group;
         const uint32_t fb = bar_full + 8 * s;
@@ -171,6 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(bar_full + 8 * s, ph);
         mbar_wait(bar_afull + 8 * a, aph);
         tc_fence_after();
+        if (i < 32) TM_TRACE(99 + i);
         const uint32_t act = act0 + s * Cfg::ACT_BYTES;
 #pragma unroll
         for (int j = 0; j < kBK / 16; ++j) {
@@ -194,6 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int a = i % ASTAGES;
       const uint32_t aph = (i / ASTAGES) & 1;
       mbar_wait(bar_full + 8 * s, ph);
+      if (i < 32 && warp == 2 && lane == 0) TM_TRACE(35 + i);
       const uint8_t* blob = blob_ptr0 + s * kBlobBytes;
       const uint4 w0 = *reinterpret_cast<const uint4*>(blob + row * 16);
       const uint4 w1 = *reinterpret_cast<const uint4*>(blob + 2048 + row * 16);
@@ -217,11 +240,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_wait_st();
       tc_fence_before();
       mbar_arrive(bar_afull + 8 * a);
+      if (i < 32 && warp == 2 && lane == 0) TM_TRACE(67 + i);
     }
 
     // ------------------------------------------------------------ epilogue
     mbar_wait(bar_acc, 0);
     tc_fence_after();
+    if (warp == 2 && lane == 0) TM_TRACE(131);
     const int n = nt * kBN + row;
     if (S > 1 && rank != 0) {
       // wait until rank 0 has drained its ring, then push fp32 partials into its SMEM
@@ -284,9 +309,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     cluster_arrive();
     cluster_wait();
   }
+  if (warp == 2 && lane == 0) TM_TRACE(132);
   grid_dependency_launch();
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) TM_TRACE(133);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::TMEM_COLS);

@@ -205,3 +205,39 @@ def test_m_zero_is_noop_and_errors():
     bad = api.PackedW4(p.data, 256, 256, 128)  # descriptor never filled by tm_pack_w4
     with pytest.raises(api.TMError, match="INVALID_ARG"):
         api.gemm_w4a16(t["A"], bad, t["s"], t["z"])
+
+
+SK_CASES = [(16, 1), (16, 3), (16, 7), (16, 148), (32, 5), (64, 4), (64, 148), (128, 3), (256, 2), (16, 2000)]
+
+
+@pytest.mark.parametrize("tile,P", SK_CASES)
+@pytest.mark.parametrize("group", [64, 128])
+def test_streamk_variants_ragged(tile, P, group):
+    """Persistent stream-K kernel with forced CTA counts P (partial tiles at every range
+    boundary), ragged M, and K not a multiple of the 256-k chunk (partial last chunk)."""
+    api.set_gemm_override(tile, -P)
+    for M, N, K in ((1, 384, 832), (tile, 256, 1024), (tile + 3, 512, 576), (2 * tile + 1, 384, 1344)):
+        d = synth.awq_like(M, N, K, group=group, seed=M * 7 + N + K + P)
+        C, _, _ = _run(d)
+        _assert_parity(C, d, tag=(tile, P, M, N, K))
+
+
+def test_streamk_partial_f32_and_fp16():
+    api.set_gemm_override(16, -5)
+    d = synth.awq_like(9, 384, 1024, seed=77)
+    C, _, _ = _run(d, out="f32")
+    _assert_parity(C, d, act="fp32")
+    d16 = synth.awq_like(9, 384, 1024, seed=78, act_dtype="fp16")
+    C16, _, _ = _run(d16, act="fp16")
+    _assert_parity(C16, d16, act="fp16")
+
+
+def test_streamk_deterministic_and_counter_reset():
+    """Repeated launches (counters must return to zero) give identical bits."""
+    api.set_gemm_override(16, -37)
+    d = synth.awq_like(16, 2048, 4096, seed=88)
+    t = to_dev(d)
+    p = api.pack_w4(t["q"], t["s"], t["z"], 128)
+    outs = [bits16(api.gemm_w4a16(t["A"], p, t["s"], t["z"])) for _ in range(4)]
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
+    _assert_parity(api.gemm_w4a16(t["A"], p, t["s"], t["z"]), d)
