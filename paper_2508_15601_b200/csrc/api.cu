@@ -14,6 +14,7 @@
 #include "aux_kernels.cuh"
 #include "gemm_w4a16.cuh"
 #include "gemm_sk.cuh"
+#include "gemm_dec.cuh"
 
 namespace {
 
@@ -381,12 +382,65 @@ tm_status launch_sk_t(const void* A, const GemmArgs& g, const Config& c, cudaStr
   return TM_OK;
 }
 
+template <int NT, bool BF16, int OUT>
+tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream) {
+  using Cfg = DecCfg<NT>;
+  auto kern = w4a16_dec_kernel<NT, BF16, OUT>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return TM_ERR_CUDA;
+    }
+    configured = true;
+  }
+  CUtensorMap ma, ms, mz;
+  tm_status st = act_tensor_map_3d(A, g.M, g.K, NT, Cfg::BLOBS, BF16, &ma);
+  if (st != TM_OK) return st;
+  st = sz_tensor_map(g.scales, g.K / g.group, g.N, &ms);
+  if (st != TM_OK) return st;
+  st = sz_tensor_map(g.zeros, g.K / g.group, g.N, &mz);
+  if (st != TM_OK) return st;
+  DecArgs a;
+  a.packed = g.packed;
+  a.out = g.out;
+  a.M = g.M;
+  a.N = g.N;
+  a.K = g.K;
+  a.group = g.group;
+  a.n_tiles = g.N / 128;
+  a.m_tiles = (g.M + NT - 1) / NT;
+  a.kc = (g.K + Cfg::CH - 1) / Cfg::CH;
+  a.total = static_cast<long long>(a.m_tiles) * a.n_tiles * a.kc;
+  a.trace = g_trace;
+  if (a.m_tiles * a.n_tiles > 65536) return TM_ERR_UNSUPPORTED_SHAPE;
+  st = get_workspace(stream, static_cast<size_t>(2) * c.split * NT * 128 * sizeof(float), a.m_tiles * a.n_tiles,
+                     &a.counters, &a.workspace);
+  if (st != TM_OK) return st;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(c.split, 1, 1);
+  cfg.blockDim = dim3(kDecThreads, 1, 1);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, ms, mz, a);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return TM_ERR_CUDA;
+  }
+  return TM_OK;
+}
+
 template <bool BF16, int OUT>
 tm_status launch_sk(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream) {
   switch (c.NT) {
-    case 16: return launch_sk_t<16, BF16, OUT>(A, g, c, stream);
-    case 32: return launch_sk_t<32, BF16, OUT>(A, g, c, stream);
-    case 64: return launch_sk_t<64, BF16, OUT>(A, g, c, stream);
+    case 16: return launch_dec_t<16, BF16, OUT>(A, g, c, stream);
+    case 32: return launch_dec_t<32, BF16, OUT>(A, g, c, stream);
+    case 64: return launch_dec_t<64, BF16, OUT>(A, g, c, stream);
     case 128: return launch_sk_t<128, BF16, OUT>(A, g, c, stream);
     case 256: return launch_sk_t<256, BF16, OUT>(A, g, c, stream);
     default: return TM_ERR_INVALID_ARG;

@@ -45,7 +45,9 @@ __device__ __forceinline__ void deq_word(uint32_t w, uint32_t s2, uint32_t z2, u
   constexpr uint32_t MAGIC = BF16 ? 0x43004300u : 0x64006400u;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const uint32_t x = ((w >> (4 * i)) & 0x000F000Fu) | MAGIC;
+    // one LOP3: (w' & 0x000F000F) | MAGIC  (LUT 0xEA = (a & b) | c)
+    uint32_t x;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(x) : "r"(w >> (4 * i)), "r"(0x000F000Fu), "r"(MAGIC));
     uint32_t d;
     if constexpr (BF16) {
       asm("{\n\t.reg .b32 t;\n\tsub.rn.bf16x2 t, %1, %2;\n\tmul.rn.bf16x2 %0, t, %3;\n\t}"

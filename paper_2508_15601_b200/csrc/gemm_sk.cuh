@@ -58,7 +58,8 @@ struct SkCfg {
   static constexpr int SZG = 8;                       // groups per s/z box
   static constexpr int SZ_BOX = SZG * 128 * 2;        // bytes of one s (or z) box
   static constexpr int SZ_SLOTS = 2;
-  static constexpr int ASTAGES = 4;                   // TMEM A stages (one blob = 32 columns)
+  static constexpr int ASTAGES = NT <= 64 ? 12 : 8;   // TMEM A stages (one blob = 32 columns): deep
+                                                      // enough to cover the MMA commit round trip
   static constexpr int ACC_COLS = NT < 32 ? 32 : NT;  // one accumulator buffer
   static constexpr int ACC_BUFS = NT <= 128 ? 2 : 1;
   static constexpr int TMEM_NEED = ACC_BUFS * ACC_COLS + ASTAGES * 32;
@@ -173,7 +174,8 @@ __global__ void __launch_bounds__(kSkThreads, 1)
   const uint32_t tmem_a0 = tmem_base + ACC_BUFS * Cfg::ACC_COLS;
 
   // chunks per s/z box (boxes are segment-relative, 8 groups each; a box spans whole chunks)
-  const int chunks_per_box = (Cfg::SZG * args.group) / CH;
+  const int gshift = args.group == 64 ? 6 : 7;
+  const int chunks_per_box = (Cfg::SZG << gshift) / CH;
 
   if (warp == 0) {
     // ---------------------------------------------------------------- producer W (+ s/z)
@@ -192,7 +194,7 @@ __global__ void __launch_bounds__(kSkThreads, 1)
             mbar_wait(bar_szempty + 8 * j, ((box / Cfg::SZ_SLOTS) & 1) ^ 1);
             const uint32_t fb = bar_szfull + 8 * j;
             mbar_arrive_expect_tx(fb, 2 * Cfg::SZ_BOX);
-            const int g0 = (c * CH) / args.group;
+            const int g0 = (c * CH) >> gshift;
             tma_load_2d(sz0 + j * 2 * Cfg::SZ_BOX, &tmap_s, nt * 128, g0, fb);
             tma_load_2d(sz0 + j * 2 * Cfg::SZ_BOX + Cfg::SZ_BOX, &tmap_z, nt * 128, g0, fb);
             ++box;
@@ -267,6 +269,7 @@ __global__ void __launch_bounds__(kSkThreads, 1)
             tc_commit(bar_aempty + 8 * a);
           }
           tc_commit(bar_empty + 8 * s);
+          if (i < 32) SK_TRACE(99 + i);
         }
         tc_commit(bar_accfull + 8 * b);
         u = cend;
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(kSkThreads, 1)
           if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));
           ++box;
           mbar_wait(bar_szfull + 8 * (box % Cfg::SZ_SLOTS), (box / Cfg::SZ_SLOTS) & 1);
-          g_base = (c * CH) / args.group;
+          g_base = (c * CH) >> gshift;
         }
         const uint8_t* szs = sz_ptr0 + (box % Cfg::SZ_SLOTS) * 2 * Cfg::SZ_BOX;
         const int s = i % STAGES;
@@ -308,15 +311,18 @@ __global__ void __launch_bounds__(kSkThreads, 1)
           }
         }
         mbar_arrive(bar_empty + 8 * s);  // codes are in registers; the MMA commit covers the activations
+        // software pipeline: the tcgen05.st of blob b completes while blob b+1 is dequantised
+        uint32_t ra[32], rb[32];
+        int pend = -1;
 #pragma unroll
         for (int bb = 0; bb < Cfg::BLOBS; ++bb) {
           if (bb < nb) {
-            const int gi = ((kb0 + bb) * 64) / args.group - g_base;
+            uint32_t(&r)[32] = (bb & 1) ? rb : ra;
+            const int gi = (((kb0 + bb) * 64) >> gshift) - g_base;
             const uint16_t sb = *reinterpret_cast<const uint16_t*>(szs + gi * 256 + row * 2);
             const uint16_t zb = *reinterpret_cast<const uint16_t*>(szs + Cfg::SZ_BOX + gi * 256 + row * 2);
             uint32_t s2, z2;
             deq_prepare<BF16>(sb, zb, s2, z2);
-            uint32_t r[32];
             deq_word<BF16>(wv[2 * bb].x, s2, z2, r + 0);
             deq_word<BF16>(wv[2 * bb].y, s2, z2, r + 4);
             deq_word<BF16>(wv[2 * bb].z, s2, z2, r + 8);
@@ -325,16 +331,25 @@ __global__ void __launch_bounds__(kSkThreads, 1)
             deq_word<BF16>(wv[2 * bb + 1].y, s2, z2, r + 20);
             deq_word<BF16>(wv[2 * bb + 1].z, s2, z2, r + 24);
             deq_word<BF16>(wv[2 * bb + 1].w, s2, z2, r + 28);
+            if (pend >= 0) {
+              tc_wait_st();
+              tc_fence_before();
+              mbar_arrive(bar_afull + 8 * pend);
+            }
             const int a = ia % ASTAGES;
             mbar_wait(bar_aempty + 8 * a, ((ia / ASTAGES) & 1) ^ 1);
             tc_fence_after();
             tmem_st_32x32b_x32(tmem_a0 + a * 32 + lane_off, r);
-            tc_wait_st();
-            tc_fence_before();
-            mbar_arrive(bar_afull + 8 * a);
+            pend = a;
             ++ia;
           }
         }
+        if (pend >= 0) {
+          tc_wait_st();
+          tc_fence_before();
+          mbar_arrive(bar_afull + 8 * pend);
+        }
+        if (i < 32 && warp == 2 && lane == 0) SK_TRACE(67 + i);
       }
       u = cend;
     }

@@ -73,3 +73,13 @@ print("slowest CTA", cta, "issue", t[cta, 3:3 + nks].tolist())
 print("   data ", t[cta, 35:35 + nks].tolist())
 print("   mma  ", t[cta, 99:99 + nks].tolist())
 print("   epi", t[cta, 131:134].tolist())
+
+if t[:, 140].max() > 0:
+    n = t[:, 140].astype(float)
+    names = {136: "MMA: wait ready", 137: "MMA: wait dfree", 138: "MMA: issue", 139: "MMA: commit+sync",
+             141: "scale: wait done", 142: "scale: work", 143: "deq: wait stage", 144: "deq: LDS",
+             145: "deq: wait TMEM slot", 146: "deq: dequant+st", 147: "deq: arrive",
+             148: "deq:  math+st issue", 149: "deq:  wait::st"}
+    for k, name in names.items():
+        div = n  # counters are per handled chunk (MMA warp 0 and dequant set 0 take every other chunk)
+        print(f"per chunk {name:24s} {np.median(t[:, k] / div):8.0f} cycles")

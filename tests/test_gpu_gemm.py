@@ -10,7 +10,7 @@ import torch
 
 from oracle import compare
 from oracle.gemm import gemm_f64
-from oracle.quant import dequant_rounded
+from oracle.quant import dequant_rounded, dequant_f64
 from oracle.numerics import round_to
 from paper_2508_15601_b200 import api, synth
 from tests.gpu_helpers import to_dev, to_np64, bits16
@@ -113,15 +113,25 @@ def test_zero_weights_exact(act):
 
 
 @pytest.mark.parametrize("act", ["bf16", "fp16"])
-def test_onehot_rows_are_dequant_rows_bit_exact(act):
+@pytest.mark.parametrize("path", ["decode", "tiled"])
+def test_onehot_rows_are_dequant_rows_bit_exact(act, path):
+    """A one-hot activation row selects one dequantised weight row.  Decode path (reading
+    R6b: exact (q - z) operand, scale in fp32, one output rounding): RNE((q - z) * s).
+    Tiled path (reading R6: weights rounded to the operand dtype before the MMA): the
+    rounding sequence of oracle.quant.dequant_rounded."""
     d = synth.uniform(1, 384, 512, group=128, seed=9, act_dtype=act)
     ks = [0, 1, 63, 64, 127, 128, 300, 511]
     A = np.zeros((len(ks), 512), dtype=np.float32)
     for m, k in enumerate(ks):
         A[m, k] = 1.0
     d["A"] = A
+    if path == "tiled":
+        api.set_gemm_override(128, 1)
     C, _, _ = _run(d, act)
-    W = dequant_rounded(d["q"], d["s"], d["z"], 128, act)
+    if path == "decode":
+        W = round_to(dequant_f64(d["q"], d["s"], d["z"], 128), act)
+    else:
+        W = dequant_rounded(d["q"], d["s"], d["z"], 128, act)
     assert np.array_equal(to_np64(C), W[ks])
 
 
@@ -216,7 +226,7 @@ def test_streamk_variants_ragged(tile, P, group):
     """Persistent stream-K kernel with forced CTA counts P (partial tiles at every range
     boundary), ragged M, and K not a multiple of the 256-k chunk (partial last chunk)."""
     api.set_gemm_override(tile, -P)
-    for M, N, K in ((1, 384, 832), (tile, 256, 1024), (tile + 3, 512, 576), (2 * tile + 1, 384, 1344)):
+    for M, N, K in ((1, 384, 896), (tile, 256, 1024), (tile + 3, 512, 640), (2 * tile + 1, 384, 1408)):
         d = synth.awq_like(M, N, K, group=group, seed=M * 7 + N + K + P)
         C, _, _ = _run(d)
         _assert_parity(C, d, tag=(tile, P, M, N, K))
