@@ -53,9 +53,11 @@ def test_host_only_entry_points():
 
 def test_config_selection_host_logic():
     api.set_gemm_override(0, 0)
-    c = api.query_gemm_config(16, 4096, 4096)
-    assert c["tile_m"] == 16 and 1 <= c["split_k"] <= 8
-    assert c["grid_ctas"] == 32 * c["split_k"]
+    c = api.query_gemm_config(16, 4096, 4096)  # decode: persistent stream-K, one CTA per SM
+    assert c["tile_m"] == 16 and c["split_k"] < 0 and c["grid_ctas"] == -c["split_k"]
+    assert c["grid_ctas"] <= 32 * 16  # never more CTAs than 256-k chunks
+    c = api.query_gemm_config(1, 128, 256)
+    assert c["grid_ctas"] == 1  # one tile of one chunk
     c = api.query_gemm_config(4096, 4096, 4096)
     assert c["tile_m"] == 256 and c["split_k"] == 1 and c["grid_ctas"] == 32 * 16
     api.set_gemm_override(64, 3)
