@@ -342,7 +342,11 @@ def bench_ours(args):
     peaks = load_peaks()
     h2d = sum(io[(M, n)]["A"].numel() * 2 for M in ms for n, _, _ in SHAPES) * L
     d2h = sum(io[(M, n)]["C"].numel() * 2 for M in ms for n, _, _ in SHAPES) * L
-    detail = per_shape_detail(layers, io, ms) if world == 1 else None
+    if world == 1:
+        with torch.cuda.stream(stream):  # same stream: reuses its stream-K workspace
+            detail = per_shape_detail(layers, io, ms)
+    else:
+        detail = None
     traffic = ncu_traffic(ms, L)
     gemm_launches = len(ms) * L * len(SHAPES)
     res = dict(
