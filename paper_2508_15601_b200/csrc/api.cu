@@ -419,7 +419,7 @@ tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaSt
   if (st != TM_OK) return st;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(c.split, 1, 1);
-  cfg.blockDim = dim3(kDecThreads, 1, 1);
+  cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attrs[1];

@@ -23,15 +23,18 @@
 //     own TMA completion into that hand-over, and the weight ring (freed by the dequant
 //     warps alone) is decoupled from the activation/TMEM ring (freed by the MMA commits).
 //
-// Warps (512 threads):
-//   0       producer W : weight chunks (1-D bulk, before griddepcontrol.wait) + s/z boxes
-//   1, 2    MMA        : issuer j takes every other chunk (all its groups); D_g -> TMEM slots
-//   3       producer A : activation chunk (3-D TMA, SW128) after griddepcontrol.wait; when
-//                        it lands, arrives on the chunk's "operands ready" barrier
-//   4..7    dequant 0  : blobs 0,1 of every chunk; thread = weight column = TMEM lane;
-//   12..15  dequant 1  : blobs 2,3.  LDS.128, LOP3 magic + exact sub, tcgen05.st
-//   8..11   scale/epi  : tcgen05.ld D_g, acc[m] += s * D_g[m] (fp32 registers); at a segment
-//                        end: RNE store of C, or fp32 partial + deterministic stream-K fix-up
+// Warps (32 x (8 + 4 NDS) threads):
+//   0        producer W : weight chunks (1-D bulk, before griddepcontrol.wait), freed by the dequant
+//   1, 2     MMA        : issuer j takes chunks i with i % NISSUE == j (all groups); D_g -> TMEM
+//   3        producer A : s/z boxes (2-D TMA), activation chunks (3-D TMA, SW128) after
+//                         griddepcontrol.wait, freed by the MMA commit
+//   4..7     scale/epi  : tcgen05.ld D_g, acc[m] += s * D_g[m] (fp32 registers); at a segment
+//                         end: RNE store of C, or fp32 partial + deterministic stream-K fix-up
+//   8 + 4j.. dequant j  : NDS sets of 4 warps; set j takes chunks i with i % NDS == j and owns
+//                         TMEM operand slot j; thread = weight column = TMEM lane; LDS.128,
+//                         LOP3 magic + exact sub, tcgen05.st
+// Per chunk: one full wait and one ready arrive (dequant), one ready wait + one D-slot wait +
+// one commit (MMA), one done wait + one D-slot release (scale).
 #pragma once
 #include <cstdint>
 #include <cuda.h>
@@ -43,7 +46,6 @@
 
 namespace w4k {
 
-constexpr int kDecThreads = 512;
 
 struct DecArgs {
   const uint8_t* packed;  // LAYOUT v1
@@ -63,20 +65,22 @@ struct DecCfg {
   static constexpr int BLOBS = 4;                        // LAYOUT v1 blobs per chunk
   static constexpr int ACT_BYTES = NT * CH * 2;          // activation chunk (4 SW128 sub-tiles)
   static constexpr int W_BYTES = BLOBS * 4096;           // packed weight chunk
-  static constexpr int STAGE_BYTES = ACT_BYTES + W_BYTES;
-  static constexpr int NR = NT <= 32 ? 6 : 4;            // stage ring = per-chunk barrier ring
-  static constexpr int AC = NT <= 16 ? 3 : 2;            // TMEM operand ring (chunks of 128 columns)
+  static constexpr int NW = NT <= 16 ? 8 : (NT <= 32 ? 6 : 5);  // weight ring (freed after the dequant's LDS)
+  static constexpr int NA = NT <= 32 ? 6 : 3;            // activation ring = per-chunk ready/done ring
+  static constexpr int NDS = NT <= 16 ? 3 : 2;           // dequant sets = TMEM operand slots
   static constexpr int DCOLS = NT;                       // one D_g slot
-  static constexpr int DCHUNK_MAX = 4 * NT;              // D columns of one chunk (g = 64: 4 groups)
-  static constexpr int DR = (512 - AC * BLOBS * 32) / DCHUNK_MAX >= 2 ? 2 : 1;  // D ring (chunks)
+  static constexpr int DCHUNK = 4 * NT;                  // D columns of one chunk (g = 64: 4 groups)
+  static constexpr int DR = (512 - NDS * BLOBS * 32) / DCHUNK >= 2 ? 2 : 1;  // D ring (chunks)
+  static constexpr int NISSUE = DR >= 2 ? 2 : 1;         // MMA issuers (each owns a D ring entry)
+  static constexpr int THREADS = 32 * (8 + 4 * NDS);     // a multiple of 4 warps (per-SMSP registers)
   static constexpr int SZG = 8;
   static constexpr int SZ_BOX = SZG * 128 * 2;
-  static constexpr int SZ_SLOTS = 2;
+  static constexpr int SZ_SLOTS = 4;                     // s/z boxes in flight (16 chunks of look-ahead)
   static constexpr int TMEM_COLS = 512;
   static constexpr int HDR = 1024;
-  static constexpr int SMEM = 1024 + HDR + NR * STAGE_BYTES + SZ_SLOTS * 2 * SZ_BOX;
-  static_assert(AC * BLOBS * 32 + DR * DCHUNK_MAX <= TMEM_COLS, "TMEM");
-  static_assert(NR >= AC, "barrier ring must cover the TMEM ring");
+  static constexpr int SMEM = 1024 + HDR + NW * W_BYTES + NA * ACT_BYTES + SZ_SLOTS * 2 * SZ_BOX;
+  static_assert(NDS * BLOBS * 32 + DR * DCHUNK <= TMEM_COLS, "TMEM");
+  static_assert(NA >= NDS && NA % NISSUE == 0, "rings");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
@@ -93,12 +97,8 @@ __device__ __forceinline__ void deq_word_int(uint32_t w, uint32_t z2, uint32_t* 
   constexpr uint32_t MAGIC = BF16 ? 0x43004300u : 0x64006400u;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    // w >> 4i: i = 1, 2 on the ALU pipe (SHF), i = 3 as IMAD.HI (w * 2^20) >> 32 on the FMA pipe,
-    // which balances the two pipes (6 ALU + 5 FMA-pipe ops per word)
-    uint32_t ws = w;
-    if (i == 1) ws = w >> 4;
-    if (i == 2) ws = w >> 8;
-    if (i == 3) asm("mul.hi.u32 %0, %1, %2;" : "=r"(ws) : "r"(w), "r"(1u << 20));
+    // w >> 4i on the ALU pipe (SHF); mul.hi was measured at half rate, so no FMA-pipe shifts
+    const uint32_t ws = w >> (4 * i);
     uint32_t x;
     asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(x) : "r"(ws), "r"(0x000F000Fu), "r"(MAGIC));
     uint32_t d;
@@ -130,10 +130,40 @@ __device__ __forceinline__ void dec_store(void* out, int N, int m, int n, float 
   }
 }
 
-#define DEC_TRACE(slot)                                                                               \
-  do {                                                                                                \
+// ring position (slot, phase) advanced without division
+struct RingPos {
+  int slot = 0;
+  uint32_t phase = 0;
+  __device__ __forceinline__ void advance(int n) {
+    if (++slot == n) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
+#ifndef TM_PROFILE
+#define TM_PROFILE 0
+#endif
+#if TM_PROFILE
+// per-thread accumulators in registers, flushed once at kernel end (a global read-modify-write
+// per event would put its own latency inside the measured intervals)
+#define DCLK() clock64()
+#define DACC(slot, v) (prof[(slot) - 136] += static_cast<uint32_t>(v))
+// timeline marks: cycles since CTA start (slot 0 = %globaltimer low bits at CTA start)
+#define DMARK(slot)                                                                             \
+  do {                                                                                          \
     if (args.trace) args.trace[blockIdx.x * 160 + (slot)] = static_cast<uint32_t>(clock64() - t_start); \
   } while (0)
+#else
+#define DMARK(slot) \
+  do {              \
+  } while (0)
+#define DCLK() 0ll
+#define DACC(slot, v) \
+  do {                \
+  } while (0)
+#endif
 
 // Iterate the CTA's segments: a segment is the part of one (m-tile, n-tile) inside [u0, u1).
 #define DEC_FOR_SEGMENTS                                                                            \
@@ -142,34 +172,47 @@ __device__ __forceinline__ void dec_store(void* out, int N, int m, int n, float 
       if ((cend = ((static_cast<long long>(t) + 1) * kc < u1 ? (static_cast<long long>(t) + 1) * kc : u1)), true)
 
 template <int NT, bool BF16, int OUT>
-__global__ void __launch_bounds__(kDecThreads, 1)
+__global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
     w4a16_dec_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_s,
                      const __grid_constant__ CUtensorMap tmap_z, const DecArgs args) {
   using Cfg = DecCfg<NT>;
-  constexpr int NR = Cfg::NR;  // stages and per-chunk full/ready/done barriers
-  constexpr int AC = Cfg::AC;
+  constexpr int NR = Cfg::NA;  // activation slots and per-chunk ready/done barriers
+  constexpr int NW = Cfg::NW;
+  constexpr int NDS = Cfg::NDS;
   constexpr int DR = Cfg::DR;
+  constexpr int NISSUE = Cfg::NISSUE;
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* const base_ptr = smem_raw + (base - smem_u32(smem_raw));
-  const uint32_t bar_full = base;                               // NR (W + A producers, tx)
-  const uint32_t bar_ready = bar_full + 8 * NR;                 // NR (128: the chunk's dequant set)
-  const uint32_t bar_done = bar_ready + 8 * NR;                 // NR (1 commit of the chunk's MMA issuer)
-  const uint32_t bar_dfree = bar_done + 8 * NR;                 // DR (128 scale: D slots of a chunk read)
+  const uint32_t bar_fullw = base;                              // NW (W producer, tx)
+  const uint32_t bar_emptyw = bar_fullw + 8 * NW;               // NW (128: the chunk's dequant set)
+  const uint32_t bar_fulla = bar_emptyw + 8 * NW;               // NR (A producer, tx)
+  const uint32_t bar_ready = bar_fulla + 8 * NR;                // NR (128: the chunk's dequant set)
+  const uint32_t bar_done = bar_ready + 8 * NR;                 // NR (1 commit: the chunk's MMA issuer)
+  const uint32_t bar_dfree = bar_done + 8 * NR;                 // DR (128 scale threads)
   const uint32_t bar_szfull = bar_dfree + 8 * DR;               // SZ_SLOTS (1)
-  const uint32_t bar_szempty = bar_szfull + 8 * Cfg::SZ_SLOTS;  // SZ_SLOTS (256 dequant + 128 scale)
+  const uint32_t bar_szempty = bar_szfull + 8 * Cfg::SZ_SLOTS;  // SZ_SLOTS (128 NDS dequant + 128 scale)
   const uint32_t tmem_slot = bar_szempty + 8 * Cfg::SZ_SLOTS;
   uint32_t* const tmem_slot_ptr = reinterpret_cast<uint32_t*>(base_ptr + (tmem_slot - base));
   int* const bcast = reinterpret_cast<int*>(base_ptr + (tmem_slot - base) + 16);
-  const uint32_t st0 = base + Cfg::HDR;                         // NR x [act | packed weights]
-  const uint32_t sz0 = st0 + NR * Cfg::STAGE_BYTES;             // SZ_SLOTS x [s box | z box]
-  const uint8_t* const st_ptr0 = base_ptr + Cfg::HDR;
-  const uint8_t* const sz_ptr0 = st_ptr0 + NR * Cfg::STAGE_BYTES;
+  const uint32_t w0 = base + Cfg::HDR;                          // NW x 16 KB packed weights
+  const uint32_t a0 = w0 + NW * Cfg::W_BYTES;                   // NR x activation chunk (1 KB aligned)
+  const uint32_t sz0 = a0 + NR * Cfg::ACT_BYTES;                // SZ_SLOTS x [s box | z box]
+  const uint8_t* const w_ptr0 = base_ptr + Cfg::HDR;
+  const uint8_t* const sz_ptr0 = w_ptr0 + NW * Cfg::W_BYTES + NR * Cfg::ACT_BYTES;
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
+#if TM_PROFILE
+  uint32_t prof[24] = {};
   const long long t_start = clock64();
+  if (args.trace && threadIdx.x == 0) {
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    args.trace[blockIdx.x * 160] = static_cast<uint32_t>(gt);
+  }
+#endif
 
   const int P = gridDim.x;
   const int p = blockIdx.x;
@@ -186,15 +229,19 @@ __global__ void __launch_bounds__(kDecThreads, 1)
     prefetch_tmap(&tmap_a);
     prefetch_tmap(&tmap_s);
     prefetch_tmap(&tmap_z);
+    for (int w = 0; w < NW; ++w) {
+      mbar_init(bar_fullw + 8 * w, 1);
+      mbar_init(bar_emptyw + 8 * w, 128);
+    }
     for (int r = 0; r < NR; ++r) {
-      mbar_init(bar_full + 8 * r, 2);
+      mbar_init(bar_fulla + 8 * r, 1);
       mbar_init(bar_ready + 8 * r, 128);
       mbar_init(bar_done + 8 * r, 1);
     }
     for (int d = 0; d < DR; ++d) mbar_init(bar_dfree + 8 * d, 128);
     for (int j = 0; j < Cfg::SZ_SLOTS; ++j) {
       mbar_init(bar_szfull + 8 * j, 1);
-      mbar_init(bar_szempty + 8 * j, 256 + 128);
+      mbar_init(bar_szempty + 8 * j, 128 * NDS + 128);
     }
     fence_mbar_init();
   }
@@ -206,19 +253,55 @@ __global__ void __launch_bounds__(kDecThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
-  const uint32_t tmem_a0 = tmem_base;                         // AC x 4 blobs x 32 columns
-  const uint32_t tmem_d0 = tmem_base + AC * Cfg::BLOBS * 32;  // DR x (groups of a chunk) x NT columns
+  if (threadIdx.x == 0) DMARK(1);
+  // PDL: let the next kernel in the stream start launching now; its CTAs take SMs as ours exit,
+  // and it waits (griddepcontrol.wait) before reading anything this kernel writes.
+  grid_dependency_launch();
+  const uint32_t tmem_a0 = tmem_base;                          // NDS x 4 blobs x 32 columns
+  const uint32_t tmem_d0 = tmem_base + NDS * Cfg::BLOBS * 32;  // DR x 4 groups x NT columns
 
   if (warp == 0) {
-    // ---------------------------------------------------------------- producer W (+ s/z)
+    // ---------------------------------------------------------------- producer W
     const uint64_t pol = policy_evict_first();
-    int i = 0, box = 0;
+    RingPos st;
+    int i = 0;
     DEC_FOR_SEGMENTS {
       const int nt = t % args.n_tiles;
       const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
       const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
       for (int c = c0; c < c1; ++c, ++i) {
-        if ((c - c0) % chunks_per_box == 0) {
+        const long long q0 = DCLK();
+        mbar_wait(bar_emptyw + 8 * st.slot, st.phase ^ 1u);  // the dequant of chunk i - NW read it
+        const long long q1 = DCLK();
+        const int kb0 = c * Cfg::BLOBS;
+        const int nb = (KS - kb0) < Cfg::BLOBS ? (KS - kb0) : Cfg::BLOBS;
+        const uint32_t fb = bar_fullw + 8 * st.slot;
+        if (elect_one()) {
+          mbar_arrive_expect_tx(fb, nb * 4096);
+          bulk_g2s_hint(w0 + st.slot * Cfg::W_BYTES, args.packed + (static_cast<size_t>(nt) * KS + kb0) * 4096,
+                        nb * 4096, fb, pol);
+        }
+        __syncwarp();
+        st.advance(NW);
+        if (lane == 0) {
+          DACC(150, q1 - q0);
+          DACC(151, DCLK() - q1);
+          DACC(152, 1);
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // ---------------------------------------------------------------- producer A (+ s/z boxes)
+    RingPos st, prev;
+    int i = 0, box = 0;
+    bool waited_dep = false;
+    DEC_FOR_SEGMENTS {
+      const int mt = t / args.n_tiles;
+      const int nt = t % args.n_tiles;
+      const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
+      const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
+      for (int c = c0; c < c1; ++c, ++i) {
+        if ((c - c0) % chunks_per_box == 0) {  // s/z do not depend on the previous kernel
           const int j = box % Cfg::SZ_SLOTS;
           mbar_wait(bar_szempty + 8 * j, ((box / Cfg::SZ_SLOTS) & 1) ^ 1);
           const uint32_t fb = bar_szfull + 8 * j;
@@ -231,145 +314,133 @@ __global__ void __launch_bounds__(kDecThreads, 1)
           __syncwarp();
           ++box;
         }
-        const int r = i % NR;
-        if (i >= NR) mbar_wait(bar_done + 8 * r, ((i - NR) / NR) & 1);  // chunk i - NR fully consumed
-        const int kb0 = c * Cfg::BLOBS;
-        const int nb = (KS - kb0) < Cfg::BLOBS ? (KS - kb0) : Cfg::BLOBS;
-        const uint32_t fb = bar_full + 8 * r;
-        if (elect_one()) {
-          mbar_arrive_expect_tx(fb, nb * 4096);
-          bulk_g2s_hint(st0 + r * Cfg::STAGE_BYTES + Cfg::ACT_BYTES,
-                        args.packed + (static_cast<size_t>(nt) * KS + kb0) * 4096, nb * 4096, fb, pol);
+        if (!waited_dep) {
+          grid_dependency_wait();  // activations may come from the previous kernel
+          waited_dep = true;
         }
-        __syncwarp();
-        if (lane == 0 && i < 32) DEC_TRACE(3 + i);
-      }
-    }
-  } else if (warp == 3) {
-    // ---------------------------------------------------------------- producer A
-    grid_dependency_wait();  // activations may come from the previous kernel
-    int i = 0;
-    DEC_FOR_SEGMENTS {
-      const int mt = t / args.n_tiles;
-      const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
-      const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
-      for (int c = c0; c < c1; ++c, ++i) {
-        const int r = i % NR;
-        if (i >= NR) mbar_wait(bar_done + 8 * r, ((i - NR) / NR) & 1);
-        const uint32_t fb = bar_full + 8 * r;
+        const long long q0 = DCLK();
+        if (i >= NR) {
+          mbar_wait(bar_done + 8 * prev.slot, prev.phase);  // MMA of chunk i - NR read the slot
+          prev.advance(NR);
+        }
+        const long long q1 = DCLK();
+        const uint32_t fb = bar_fulla + 8 * st.slot;
         if (elect_one()) {
           mbar_arrive_expect_tx(fb, Cfg::ACT_BYTES);
-          tma_load_3d(st0 + r * Cfg::STAGE_BYTES, &tmap_a, 0, mt * NT, c * Cfg::BLOBS, fb);
+          tma_load_3d(a0 + st.slot * Cfg::ACT_BYTES, &tmap_a, 0, mt * NT, c * Cfg::BLOBS, fb);
         }
         __syncwarp();
+        st.advance(NR);
+        if (lane == 0) {
+          DACC(153, q1 - q0);
+          DACC(154, DCLK() - q1);
+        }
       }
     }
   } else if (warp == 1 || warp == 2) {
     // ---------------------------------------------------------------- MMA issuers
-    // whole warp runs the loop (warp-uniform operands); one elected lane issues.  Per chunk:
-    // wait ready, wait D ring slot, MMAs of my groups, one commit on done.
+    // whole warp runs the loop (warp-uniform operands); one elected lane issues.  Issuer j takes
+    // chunks i % NISSUE == j (all groups) and always uses D ring entry j (NISSUE == DR or 1).
+    // (Splitting a chunk's MMAs between both issuers was measured slower: concurrent issuers
+    // each slow to ~87 cycles per MMA, i.e. the SM completes one M=128,N=16 MMA per ~44 cycles.)
     const int me = warp - 1;
-    constexpr int NISSUE = DR >= 2 ? 2 : 1;
     constexpr uint32_t idesc = umma_idesc_f16(BF16, 128, NT);
-    int i = 0;
-    DEC_FOR_SEGMENTS {
-      const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
-      const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
-      for (int c = c0; c < c1; ++c, ++i) {
-        // issuer j takes chunks i with i % NISSUE == j (all groups); two alternating issuers need
-        // two D ring entries, otherwise a fast issuer could alias a dfree phase
-        if (i % NISSUE != me) continue;
-        const int r = i % NR;
-        const int ac = i % AC;
-        const int dr = i % DR;
-        const int kb0 = c * Cfg::BLOBS;
-        const int nb = (KS - kb0) < Cfg::BLOBS ? (KS - kb0) : Cfg::BLOBS;
-        const int ng = nb / bpg;
-        const uint32_t act = st0 + r * Cfg::STAGE_BYTES;
-        const long long q0 = clock64();
-        mbar_wait(bar_ready + 8 * r, (i / NR) & 1);        // operands in TMEM, activations in SMEM
-        const long long q1 = clock64();
-        mbar_wait(bar_dfree + 8 * dr, ((i / DR) & 1) ^ 1);  // D slots of this ring entry read
-        tc_fence_after();
-        const long long q2 = clock64();
-        long long q3 = q2;
-        if (elect_one()) {
-          for (int g = 0; g < ng; ++g) {
-            const uint32_t d_tmem = tmem_d0 + (dr * 4 + g) * Cfg::DCOLS;
-            for (int bb = 0; bb < bpg; ++bb) {
-              const int blob = g * bpg + bb;
-              const uint32_t a_tmem = tmem_a0 + (ac * Cfg::BLOBS + blob) * 32;
-              const uint64_t bdesc0 = umma_desc_sw128(act + blob * (NT * 128));
+    if (me < NISSUE) {
+      int i = 0;
+      DEC_FOR_SEGMENTS {
+        const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
+        const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
+        for (int c = c0; c < c1; ++c, ++i) {
+          if (i % NISSUE != me) continue;
+          const int r = i % NR;
+          const uint32_t rph = (i / NR) & 1;
+          const int ac = i % NDS;
+          const int dr = i % DR;
+          const int kb0 = c * Cfg::BLOBS;
+          const int nb = (KS - kb0) < Cfg::BLOBS ? (KS - kb0) : Cfg::BLOBS;
+          const int ng = nb / bpg;
+          const uint32_t act = a0 + r * Cfg::ACT_BYTES;
+          const long long q0 = DCLK();
+          mbar_wait(bar_fulla + 8 * r, rph);                    // activations in SMEM
+          mbar_wait(bar_ready + 8 * r, rph);                    // operands in TMEM
+          const long long q1 = DCLK();
+          mbar_wait(bar_dfree + 8 * dr, ((i / DR) & 1) ^ 1);    // D slots of this ring entry read
+          tc_fence_after();
+          const long long q2 = DCLK();
+          long long q3 = q2;
+          if (elect_one()) {
+            for (int g = 0; g < ng; ++g) {
+              const uint32_t d_tmem = tmem_d0 + (dr * 4 + g) * Cfg::DCOLS;
+              for (int bb = 0; bb < bpg; ++bb) {
+                const int blob = g * bpg + bb;
+                const uint32_t a_tmem = tmem_a0 + (ac * Cfg::BLOBS + blob) * 32;
+                const uint64_t bdesc0 = umma_desc_sw128(act + blob * (NT * 128));
 #pragma unroll
-              for (int j = 0; j < 4; ++j)
-                mma_ts(d_tmem, a_tmem + 8 * j, bdesc0 + 2 * j, idesc, (bb | j) != 0 ? 1u : 0u);
+                for (int j = 0; j < 4; ++j)
+                  mma_ts(d_tmem, a_tmem + 8 * j, bdesc0 + 2 * j, idesc, (bb | j) != 0 ? 1u : 0u);
+              }
             }
+            q3 = DCLK();
+            tc_commit(bar_done + 8 * r);
           }
-          q3 = clock64();
-          tc_commit(bar_done + 8 * r);
+          __syncwarp();
+          if (me == 0 && lane == 0) {
+            DACC(136, q1 - q0);
+            DACC(137, q2 - q1);
+            DACC(138, q3 - q2);
+            DACC(139, DCLK() - q3);
+            DACC(140, 1);
+          }
         }
-        __syncwarp();
-        if (args.trace && me == 0 && lane == 0) {  // per-role cycle accounting (debug)
-          uint32_t* tr = args.trace + blockIdx.x * 160;
-          tr[136] += static_cast<uint32_t>(q1 - q0);
-          tr[137] += static_cast<uint32_t>(q2 - q1);
-          tr[138] += static_cast<uint32_t>(q3 - q2);
-          tr[139] += static_cast<uint32_t>(clock64() - q3);
-          tr[140] += 1;
-        }
-        if (me == 0 && lane == 0 && i < 32) DEC_TRACE(99 + i);
       }
     }
-  } else if ((warp >= 4 && warp <= 7) || warp >= 12) {
-    // ---------------------------------------------------------------- dequant (2 sets)
-    // set j takes whole chunks i with i % 2 == j, so one set's waits overlap the other's work
-    const int set = warp >= 12 ? 1 : 0;
+  } else if (warp >= 8) {
+    // ---------------------------------------------------------------- dequant (NDS sets)
+    const int set = (warp - 8) >> 2;  // takes chunks i % NDS == set, TMEM operand slot `set`
     const int quarter = warp & 3;
     const int row = quarter * 32 + static_cast<int>(lane);
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-    int i = 0, box = -1;
+    const uint32_t a_slot = tmem_a0 + set * Cfg::BLOBS * 32 + lane_off;
+    int i = 0, box = -1, mine = 0;
+    bool box_ready = false;
     DEC_FOR_SEGMENTS {
       const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
       const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
       int g_base = 0;
       for (int c = c0; c < c1; ++c, ++i) {
         if ((c - c0) % chunks_per_box == 0) {
-          if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));
+          if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));  // leaving box
           ++box;
-          mbar_wait(bar_szfull + 8 * (box % Cfg::SZ_SLOTS), (box / Cfg::SZ_SLOTS) & 1);
+          box_ready = false;
           g_base = (c * Cfg::CH) >> gshift;
         }
-        if ((i & 1) != set) continue;
+        if (i % NDS != set) continue;
+        if (!box_ready) {  // wait for the box only before a chunk this set owns
+          mbar_wait(bar_szfull + 8 * (box % Cfg::SZ_SLOTS), (box / Cfg::SZ_SLOTS) & 1);
+          box_ready = true;
+        }
         const uint8_t* zs = sz_ptr0 + (box % Cfg::SZ_SLOTS) * 2 * Cfg::SZ_BOX + Cfg::SZ_BOX;
         const int r = i % NR;
-        const int ac = i % AC;
+        const int ws = i % NW;
         const int kb0 = c * Cfg::BLOBS;
         const int nb = (KS - kb0) < Cfg::BLOBS ? (KS - kb0) : Cfg::BLOBS;
-        const long long q0 = clock64();
-        mbar_wait(bar_full + 8 * r, (i / NR) & 1);  // weights and activations of the chunk landed
-        const long long q1 = clock64();
-        if (i < 32 && warp == 4 && lane == 0) DEC_TRACE(35 + i);
-        const uint8_t* wst = st_ptr0 + r * Cfg::STAGE_BYTES + Cfg::ACT_BYTES + row * 16;
-        // codes of blob 0 now; each later blob is loaded one step ahead of its use, so only
-        // two 16-byte vectors are live and the two 32-register operand buffers get their own
-        // ranges (tcgen05.st reads its source registers asynchronously)
+        const long long q0 = DCLK();
+        mbar_wait(bar_fullw + 8 * ws, (i / NW) & 1);  // the chunk's packed weights landed
+        const long long q1 = DCLK();
+        if (i == 0 && warp == 8 && lane == 0) DMARK(2);
+        const uint8_t* wst = w_ptr0 + ws * Cfg::W_BYTES + row * 16;
         uint4 wa = *reinterpret_cast<const uint4*>(wst);
         uint4 wb = *reinterpret_cast<const uint4*>(wst + 2048);
-        const long long q2 = clock64();
-        if (i >= AC) mbar_wait(bar_done + 8 * ((i - AC) % NR), ((i - AC) / NR) & 1);  // TMEM slot free
+        // this set's TMEM slot was last read by the MMA of chunk i - NDS
+        if (mine > 0) {
+          const int ip = i - NDS;
+          mbar_wait(bar_done + 8 * (ip % NR), (ip / NR) & 1);
+        }
         tc_fence_after();
-        const long long q3 = clock64();
-        uint32_t ra[32], rb[32];
-        long long qa = q3, qb = q3;
+        const long long q2 = DCLK();
 #pragma unroll
         for (int bb = 0; bb < 4; ++bb) {
           if (bb < nb) {
-            uint32_t(&rr)[32] = (bb & 1) ? rb : ra;
-            if (bb == 2) {
-              qa = clock64();
-              tc_wait_st();  // ra is rewritten: its tcgen05.st must have completed
-              qb = clock64();
-            }
             const uint4 xa = wa, xb = wb;
             if (bb + 1 < nb) {
               wa = *reinterpret_cast<const uint4*>(wst + (bb + 1) * 4096);
@@ -377,6 +448,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
             }
             const int gi = (((kb0 + bb) * 64) >> gshift) - g_base;
             const uint32_t z2 = zero_operand<BF16>(*reinterpret_cast<const uint16_t*>(zs + gi * 256 + row * 2));
+            uint32_t rr[32];
             deq_word_int<BF16>(xa.x, z2, rr + 0);
             deq_word_int<BF16>(xa.y, z2, rr + 4);
             deq_word_int<BF16>(xa.z, z2, rr + 8);
@@ -385,35 +457,30 @@ __global__ void __launch_bounds__(kDecThreads, 1)
             deq_word_int<BF16>(xb.y, z2, rr + 20);
             deq_word_int<BF16>(xb.z, z2, rr + 24);
             deq_word_int<BF16>(xb.w, z2, rr + 28);
-            tmem_st_32x32b_x32(tmem_a0 + (ac * Cfg::BLOBS + bb) * 32 + lane_off, rr);
-            if (bb >= 1) keep_alive_32((bb & 1) ? ra : rb);  // previous buffer: live until here
+            tmem_st_32x32b_x32(a_slot + bb * 32, rr);
           }
         }
-        const long long qc = clock64();
+        mbar_arrive(bar_emptyw + 8 * ws);  // all LDS of the chunk's codes have completed
         tc_wait_st();
         tc_fence_before();
-        const long long q4 = clock64();
         mbar_arrive(bar_ready + 8 * r);
-        if (args.trace && warp == 4 && lane == 0) {
-          uint32_t* tr = args.trace + blockIdx.x * 160;
-          tr[143] += static_cast<uint32_t>(q1 - q0);  // wait stage
-          tr[144] += static_cast<uint32_t>(q2 - q1);  // LDS
-          tr[145] += static_cast<uint32_t>(q3 - q2);  // wait TMEM slot
-          tr[146] += static_cast<uint32_t>(q4 - q3);  // dequant + st
-          tr[147] += static_cast<uint32_t>(clock64() - q4);
-          tr[148] += static_cast<uint32_t>((qa - q3) + (qc - qb));  // dequant math + st issue
-          tr[149] += static_cast<uint32_t>((qb - qa) + (q4 - qc));  // tcgen05.wait::st
+        if (lane == 0 && (warp & 3) == 0) DMARK(3);  // last chunk's operands written (latest wins)
+        ++mine;
+        if (warp == 8 && lane == 0) {
+          DACC(143, q1 - q0);
+          DACC(144, q2 - q1);
+          DACC(146, DCLK() - q2);
+          DACC(148, 1);
         }
-        if (i < 32 && warp == 4 && lane == 0) DEC_TRACE(67 + i);
       }
     }
     if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));
-  } else {
+  } else if (warp >= 4 && warp < 8) {
     // ---------------------------------------------------------------- scale + epilogue
     const int quarter = warp & 3;
     const int row = quarter * 32 + static_cast<int>(lane);
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-    const int et = threadIdx.x - 8 * 32;  // 0..127
+    const int et = threadIdx.x - 4 * 32;  // 0..127 (warps 4..7)
     int ci = 0, box = -1;
     DEC_FOR_SEGMENTS {
       const int nt = t % args.n_tiles;
@@ -437,10 +504,10 @@ __global__ void __launch_bounds__(kDecThreads, 1)
         const int ng = nb / bpg;
         const int r = ci % NR;
         const int dr = ci % DR;
-        const long long q0 = clock64();
+        const long long q0 = DCLK();
         mbar_wait(bar_done + 8 * r, (ci / NR) & 1);
         tc_fence_after();
-        const long long q1 = clock64();
+        const long long q1 = DCLK();
         for (int g = 0; g < ng; ++g) {
           const int gi = ((kb0 * 64) >> gshift) + g - g_base;
           const float sc = __half2float(__ushort_as_half(*reinterpret_cast<const uint16_t*>(ss + gi * 256 + row * 2)));
@@ -455,13 +522,13 @@ __global__ void __launch_bounds__(kDecThreads, 1)
         }
         tc_fence_before();
         mbar_arrive(bar_dfree + 8 * dr);
-        if (args.trace && et == 0) {
-          uint32_t* tr = args.trace + blockIdx.x * 160;
-          tr[141] += static_cast<uint32_t>(q1 - q0);
-          tr[142] += static_cast<uint32_t>(clock64() - q1);
+        if (et == 0) {
+          DACC(141, q1 - q0);
+          DACC(142, DCLK() - q1);
         }
         ++ci;
       }
+      if (et == 0) DMARK(4);  // accumulation of this segment finished (latest segment wins)
       // ---- segment end: store (whole tile) or stream-K partial + fix-up
       const long long tile_lo = static_cast<long long>(t) * kc;
       const long long tile_hi = tile_lo + kc;
@@ -513,8 +580,18 @@ __global__ void __launch_bounds__(kDecThreads, 1)
     if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));
   }
 
-  if (threadIdx.x == 0) DEC_TRACE(133);
-  grid_dependency_launch();
+  if (warp == 4 && lane == 0) DMARK(5);  // epilogue finished
+#if TM_PROFILE
+  if (args.trace) {
+    if (threadIdx.x == 0) {
+      uint64_t gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      args.trace[blockIdx.x * 160 + 6] = static_cast<uint32_t>(gt);
+    }
+    for (int k = 0; k < 24; ++k)
+      if (prof[k]) atomicAdd(args.trace + blockIdx.x * 160 + 136 + k, prof[k]);
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {

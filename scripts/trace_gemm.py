@@ -74,12 +74,27 @@ print("   data ", t[cta, 35:35 + nks].tolist())
 print("   mma  ", t[cta, 99:99 + nks].tolist())
 print("   epi", t[cta, 131:134].tolist())
 
-if t[:, 140].max() > 0:
-    n = t[:, 140].astype(float)
-    names = {136: "MMA: wait ready", 137: "MMA: wait dfree", 138: "MMA: issue", 139: "MMA: commit+sync",
-             141: "scale: wait done", 142: "scale: work", 143: "deq: wait stage", 144: "deq: LDS",
-             145: "deq: wait TMEM slot", 146: "deq: dequant+st", 147: "deq: arrive",
-             148: "deq:  math+st issue", 149: "deq:  wait::st"}
-    for k, name in names.items():
-        div = n  # counters are per handled chunk (MMA warp 0 and dequant set 0 take every other chunk)
-        print(f"per chunk {name:24s} {np.median(t[:, k] / div):8.0f} cycles")
+if t[:, 140].max() > 0:  # built with TM_PROFILE=1
+    n = t[:, 140].astype(float)   # chunks handled by MMA issuer 0
+    nd = np.maximum(t[:, 148].astype(float), 1)  # chunks handled by dequant set 0
+    for k, name in {136: "MMA: wait ready", 137: "MMA: wait dfree", 138: "MMA: issue", 139: "MMA: commit+sync"}.items():
+        print(f"per owned chunk {name:22s} {np.median(t[:, k] / n):8.0f} cycles")
+    tot = (t[:, 141] + t[:, 142]).astype(float)
+    for k, name in {141: "scale: wait done", 142: "scale: work"}.items():
+        print(f"per chunk       {name:22s} {np.median(t[:, k] / np.maximum(n * 2, 1)):8.0f} cycles (approx)")
+    for k, name in {143: "deq: wait full", 144: "deq: LDS+wait slot", 146: "deq: math+st+arrive"}.items():
+        print(f"per owned chunk {name:22s} {np.median(t[:, k] / nd):8.0f} cycles")
+    if t[:, 152].max() > 0:
+        npc = t[:, 152].astype(float)
+        for k, name in {150: "prodW: wait done", 151: "prodW: issue", 153: "prodA: wait done", 154: "prodA: issue"}.items():
+            print(f"per chunk       {name:22s} {np.median(t[:, k] / npc):8.0f} cycles")
+    if t[:, 2].max() > 0:
+        g0 = t[:, 0]
+        print("timeline (cycles since CTA start, p50/p90/max over CTAs):")
+        for k, name in {1: "setup done", 2: "first weights landed", 3: "last operands written", 4: "last accumulation done",
+                        5: "epilogue done"}.items():
+            x = t[:, k]
+            print(f"   {name:24s} {np.percentile(x,50):8.0f} {np.percentile(x,90):8.0f} {x.max():8.0f}")
+        start_ns = (g0 - g0.min())
+        end_ns = (t[:, 6] - g0.min())
+        print(f"   CTA start spread ns: p50 {np.percentile(start_ns,50):.0f} max {start_ns.max():.0f}; CTA end (ns from first start): p50 {np.percentile(end_ns,50):.0f} max {end_ns.max():.0f}")
