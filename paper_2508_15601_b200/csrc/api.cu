@@ -174,7 +174,9 @@ tm_status sz_tensor_map(const void* p, int G, int N, CUtensorMap* out) {
 
 // ---------------------------------------------------------------- stream-K workspace
 // Per-stream device buffer: [counters: 64K ints][fp32 partial slots].  Counters are zeroed once
-// at allocation and returned to zero by the kernel's last contributor of every split tile.
+// at allocation and every kernel returns the ones it raised to zero before it exits (decode:
+// per-CTA partial flags, reset by the head holder; older stream-K: per-tile arrival counters,
+// reset by the last arriver).
 struct Workspace {
   void* ptr = nullptr;
   size_t bytes = 0;
@@ -413,9 +415,9 @@ tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaSt
   a.kc = (g.K + Cfg::CH - 1) / Cfg::CH;
   a.total = static_cast<long long>(a.m_tiles) * a.n_tiles * a.kc;
   a.trace = g_trace;
-  if (a.m_tiles * a.n_tiles > 65536) return TM_ERR_UNSUPPORTED_SHAPE;
-  st = get_workspace(stream, static_cast<size_t>(2) * c.split * NT * 128 * sizeof(float), a.m_tiles * a.n_tiles,
-                     &a.counters, &a.workspace);
+  // one partial slot and one flag per CTA (its first segment)
+  st = get_workspace(stream, static_cast<size_t>(c.split) * NT * 128 * sizeof(float), c.split, &a.counters,
+                     &a.workspace);
   if (st != TM_OK) return st;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(c.split, 1, 1);

@@ -23,16 +23,17 @@
 //     own TMA completion into that hand-over, and the weight ring (freed by the dequant
 //     warps alone) is decoupled from the activation/TMEM ring (freed by the MMA commits).
 //
-// Warps (32 x (8 + 4 NDS) threads):
-//   0        producer W : weight chunks (1-D bulk, before griddepcontrol.wait), freed by the dequant
-//   1, 2     MMA        : issuer j takes chunks i with i % NISSUE == j (all groups); D_g -> TMEM
-//   3        producer A : s/z boxes (2-D TMA), activation chunks (3-D TMA, SW128) after
-//                         griddepcontrol.wait, freed by the MMA commit
-//   4..7     scale/epi  : tcgen05.ld D_g, acc[m] += s * D_g[m] (fp32 registers); at a segment
-//                         end: RNE store of C, or fp32 partial + deterministic stream-K fix-up
-//   8 + 4j.. dequant j  : NDS sets of 4 warps; set j takes chunks i with i % NDS == j and owns
-//                         TMEM operand slot j; thread = weight column = TMEM lane; LDS.128,
-//                         LOP3 magic + exact sub, tcgen05.st
+// Warps (32 x (8 + 4 NDS) threads; ids ordered by issue priority, see DecCfg):
+//   4j..4j+3   dequant j  : NDS sets of 4 warps; set j takes chunks i with i % NDS == j and owns
+//                           TMEM operand slot j; thread = weight column = TMEM lane; LDS.128,
+//                           LOP3 magic + exact sub, tcgen05.st
+//   4NDS..+3   scale/epi  : tcgen05.ld D_g, acc[m] += s * D_g[m] (fp32 registers); at a segment
+//                           end: RNE store of C, or fp32 partial + deterministic stream-K fix-up
+//   4NDS+4,+5  MMA        : issuer j takes chunks i with i % NISSUE == j (all groups); D_g -> TMEM
+//   4NDS+6     producer A : s/z boxes (2-D TMA), activation chunks (3-D TMA, SW128) after
+//                           griddepcontrol.wait, freed by the MMA commit
+//   4NDS+7     producer W : weight chunks (1-D bulk, before griddepcontrol.wait), freed by the
+//                           dequant
 // Per chunk: one full wait and one ready arrive (dequant), one ready wait + one D-slot wait +
 // one commit (MMA), one done wait + one D-slot release (scale).
 #pragma once
@@ -50,8 +51,8 @@ namespace w4k {
 struct DecArgs {
   const uint8_t* packed;  // LAYOUT v1
   void* out;              // [M][N] bf16/fp16 or fp32
-  float* workspace;       // [2 * P][NT][128] fp32 partial slots
-  int* counters;          // [m_tiles * n_tiles] arrival counters (zero between launches)
+  float* workspace;       // [P][NT][128] fp32 partial slots (one per CTA: its first segment)
+  int* counters;          // [P] partial-ready flags (zero between launches)
   int M, N, K, group;
   int n_tiles, m_tiles;
   int kc;                 // chunks per tile = ceil(K / 256)
@@ -69,20 +70,43 @@ struct DecCfg {
   static constexpr int NA = NT <= 32 ? 6 : 3;            // activation ring = per-chunk ready/done ring
   static constexpr int NDS = NT <= 16 ? 3 : 2;           // dequant sets = TMEM operand slots
   static constexpr int DCOLS = NT;                       // one D_g slot
-  static constexpr int DCHUNK = 4 * NT;                  // D columns of one chunk (g = 64: 4 groups)
-  static constexpr int DR = (512 - NDS * BLOBS * 32) / DCHUNK >= 2 ? 2 : 1;  // D ring (chunks)
-  static constexpr int NISSUE = DR >= 2 ? 2 : 1;         // MMA issuers (each owns a D ring entry)
+  static constexpr int DAVAIL = 512 - NDS * BLOBS * 32;  // TMEM columns left for the D ring
+  static constexpr int DR_MAX = 4;                       // D ring entries (chunks); runtime: dec_dring()
   static constexpr int THREADS = 32 * (8 + 4 * NDS);     // a multiple of 4 warps (per-SMSP registers)
+  // warp roles, ordered by issue priority: the SM's warp arbiter picks the highest eligible warp
+  // id first, so the latency-critical single-thread roles get the highest ids and the ALU-bound
+  // dequant warps the lowest (measured: with the producers/MMA at ids 0-3 the MMA issuer was
+  // starved to ~47 cycles per MMA; ~20 in isolation)
+  static constexpr int W_DEQ = 0;                        // 4 * NDS dequant warps
+  static constexpr int W_SCALE = 4 * NDS;                // 4 scale / epilogue warps
+  static constexpr int W_MMA = 4 * NDS + 4;              // 2 MMA issuer warps (also TMEM allocator)
+  static constexpr int W_PRODA = 4 * NDS + 6;            // activation + s/z producer
+  static constexpr int W_PRODW = 4 * NDS + 7;            // weight producer (highest priority)
   static constexpr int SZG = 8;
   static constexpr int SZ_BOX = SZG * 128 * 2;
   static constexpr int SZ_SLOTS = 4;                     // s/z boxes in flight (16 chunks of look-ahead)
   static constexpr int TMEM_COLS = 512;
   static constexpr int HDR = 1024;
   static constexpr int SMEM = 1024 + HDR + NW * W_BYTES + NA * ACT_BYTES + SZ_SLOTS * 2 * SZ_BOX;
-  static_assert(NDS * BLOBS * 32 + DR * DCHUNK <= TMEM_COLS, "TMEM");
-  static_assert(NA >= NDS && NA % NISSUE == 0, "rings");
+  static_assert(DAVAIL >= 4 * NT, "TMEM: one chunk of g = 64 D slots");
+  static_assert(NA >= NDS, "rings");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
+
+// D ring depth for this launch: a chunk's D slots take (256 / group) * NT columns, so g = 128
+// fits twice the ring of g = 64 (more slack between the MMA and the scale warps)
+template <int NT>
+__device__ __forceinline__ int dec_dring(int group) {
+  const int per_chunk = (256 / group) * NT;
+  const int n = DecCfg<NT>::DAVAIL / per_chunk;
+  return n >= 4 ? 4 : (n >= 2 ? 2 : 1);
+}
+// MMA issuers: two when each owns whole D ring entries and whole ready/done barriers (NA even:
+// chunks sharing a barrier then share an issuer, so no parity aliasing), else one
+template <int NT>
+__device__ __forceinline__ int dec_nissue(int dring) {
+  return (dring >= 2 && DecCfg<NT>::NA % 2 == 0) ? 2 : 1;
+}
 
 __device__ __forceinline__ int dec_owner(long long u, long long T, int P) {
   return static_cast<int>(((u + 1) * P - 1) / T);
@@ -145,6 +169,11 @@ struct RingPos {
 #ifndef TM_PROFILE
 #define TM_PROFILE 0
 #endif
+// diagnostics only (wrong results): bit 0 no weight loads, bit 1 no dequant math, bit 2 no MMAs,
+// bit 3 no activation loads
+#ifndef TM_DIAG
+#define TM_DIAG 0
+#endif
 #if TM_PROFILE
 // per-thread accumulators in registers, flushed once at kernel end (a global read-modify-write
 // per event would put its own latency inside the measured intervals)
@@ -179,8 +208,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
   constexpr int NR = Cfg::NA;  // activation slots and per-chunk ready/done barriers
   constexpr int NW = Cfg::NW;
   constexpr int NDS = Cfg::NDS;
-  constexpr int DR = Cfg::DR;
-  constexpr int NISSUE = Cfg::NISSUE;
+  constexpr int DR_MAX = Cfg::DR_MAX;
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -190,19 +218,18 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
   const uint32_t bar_fulla = bar_emptyw + 8 * NW;               // NR (A producer, tx)
   const uint32_t bar_ready = bar_fulla + 8 * NR;                // NR (128: the chunk's dequant set)
   const uint32_t bar_done = bar_ready + 8 * NR;                 // NR (1 commit: the chunk's MMA issuer)
-  const uint32_t bar_dfree = bar_done + 8 * NR;                 // DR (128 scale threads)
-  const uint32_t bar_szfull = bar_dfree + 8 * DR;               // SZ_SLOTS (1)
+  const uint32_t bar_dfree = bar_done + 8 * NR;                 // DR_MAX (128 scale threads)
+  const uint32_t bar_szfull = bar_dfree + 8 * DR_MAX;           // SZ_SLOTS (1)
   const uint32_t bar_szempty = bar_szfull + 8 * Cfg::SZ_SLOTS;  // SZ_SLOTS (128 NDS dequant + 128 scale)
   const uint32_t tmem_slot = bar_szempty + 8 * Cfg::SZ_SLOTS;
   uint32_t* const tmem_slot_ptr = reinterpret_cast<uint32_t*>(base_ptr + (tmem_slot - base));
-  int* const bcast = reinterpret_cast<int*>(base_ptr + (tmem_slot - base) + 16);
   const uint32_t w0 = base + Cfg::HDR;                          // NW x 16 KB packed weights
   const uint32_t a0 = w0 + NW * Cfg::W_BYTES;                   // NR x activation chunk (1 KB aligned)
   const uint32_t sz0 = a0 + NR * Cfg::ACT_BYTES;                // SZ_SLOTS x [s box | z box]
   const uint8_t* const w_ptr0 = base_ptr + Cfg::HDR;
   const uint8_t* const sz_ptr0 = w_ptr0 + NW * Cfg::W_BYTES + NR * Cfg::ACT_BYTES;
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);  // warp-uniform
   const uint32_t lane = threadIdx.x & 31;
 #if TM_PROFILE
   uint32_t prof[24] = {};
@@ -224,8 +251,11 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
   const int gshift = args.group == 64 ? 6 : 7;
   const int bpg = args.group >> 6;  // blobs per group (1 or 2)
   const int chunks_per_box = (Cfg::SZG << gshift) / Cfg::CH;
+  const int DR = dec_dring<NT>(args.group);           // D ring entries
+  const int NISSUE = dec_nissue<NT>(DR);
+  const int DSTRIDE = (Cfg::CH >> gshift) * NT;        // D columns per ring entry
 
-  if (warp == 0 && lane == 0) {
+  if (warp == Cfg::W_PRODW && lane == 0) {
     prefetch_tmap(&tmap_a);
     prefetch_tmap(&tmap_s);
     prefetch_tmap(&tmap_z);
@@ -238,14 +268,14 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
       mbar_init(bar_ready + 8 * r, 128);
       mbar_init(bar_done + 8 * r, 1);
     }
-    for (int d = 0; d < DR; ++d) mbar_init(bar_dfree + 8 * d, 128);
+    for (int d = 0; d < DR_MAX; ++d) mbar_init(bar_dfree + 8 * d, 128);
     for (int j = 0; j < Cfg::SZ_SLOTS; ++j) {
       mbar_init(bar_szfull + 8 * j, 1);
       mbar_init(bar_szempty + 8 * j, 128 * NDS + 128);
     }
     fence_mbar_init();
   }
-  if (warp == 1) {
+  if (warp == Cfg::W_MMA) {
     tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
     tmem_relinquish();
   }
@@ -258,9 +288,9 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
   // and it waits (griddepcontrol.wait) before reading anything this kernel writes.
   grid_dependency_launch();
   const uint32_t tmem_a0 = tmem_base;                          // NDS x 4 blobs x 32 columns
-  const uint32_t tmem_d0 = tmem_base + NDS * Cfg::BLOBS * 32;  // DR x 4 groups x NT columns
+  const uint32_t tmem_d0 = tmem_base + NDS * Cfg::BLOBS * 32;  // DR x (256 / g) groups x NT columns
 
-  if (warp == 0) {
+  if (warp == Cfg::W_PRODW) {
     // ---------------------------------------------------------------- producer W
     const uint64_t pol = policy_evict_first();
     RingPos st;
@@ -276,7 +306,9 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         const int kb0 = c * Cfg::BLOBS;
         const int nb = (KS - kb0) < Cfg::BLOBS ? (KS - kb0) : Cfg::BLOBS;
         const uint32_t fb = bar_fullw + 8 * st.slot;
-        if (elect_one()) {
+        if (TM_DIAG & 1) {
+          if (elect_one()) mbar_arrive(fb);
+        } else if (elect_one()) {
           mbar_arrive_expect_tx(fb, nb * 4096);
           bulk_g2s_hint(w0 + st.slot * Cfg::W_BYTES, args.packed + (static_cast<size_t>(nt) * KS + kb0) * 4096,
                         nb * 4096, fb, pol);
@@ -290,7 +322,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         }
       }
     }
-  } else if (warp == 3) {
+  } else if (warp == Cfg::W_PRODA) {
     // ---------------------------------------------------------------- producer A (+ s/z boxes)
     RingPos st, prev;
     int i = 0, box = 0;
@@ -325,7 +357,9 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         }
         const long long q1 = DCLK();
         const uint32_t fb = bar_fulla + 8 * st.slot;
-        if (elect_one()) {
+        if (TM_DIAG & 8) {
+          if (elect_one()) mbar_arrive(fb);
+        } else if (elect_one()) {
           mbar_arrive_expect_tx(fb, Cfg::ACT_BYTES);
           tma_load_3d(a0 + st.slot * Cfg::ACT_BYTES, &tmap_a, 0, mt * NT, c * Cfg::BLOBS, fb);
         }
@@ -337,13 +371,13 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         }
       }
     }
-  } else if (warp == 1 || warp == 2) {
+  } else if (warp == Cfg::W_MMA || warp == Cfg::W_MMA + 1) {
     // ---------------------------------------------------------------- MMA issuers
     // whole warp runs the loop (warp-uniform operands); one elected lane issues.  Issuer j takes
-    // chunks i % NISSUE == j (all groups) and always uses D ring entry j (NISSUE == DR or 1).
+    // chunks i % NISSUE == j (all groups) and so always the D ring entries dr = j (mod NISSUE).
     // (Splitting a chunk's MMAs between both issuers was measured slower: concurrent issuers
     // each slow to ~87 cycles per MMA, i.e. the SM completes one M=128,N=16 MMA per ~44 cycles.)
-    const int me = warp - 1;
+    const int me = warp - Cfg::W_MMA;
     constexpr uint32_t idesc = umma_idesc_f16(BF16, 128, NT);
     if (me < NISSUE) {
       int i = 0;
@@ -369,8 +403,8 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
           const long long q2 = DCLK();
           long long q3 = q2;
           if (elect_one()) {
-            for (int g = 0; g < ng; ++g) {
-              const uint32_t d_tmem = tmem_d0 + (dr * 4 + g) * Cfg::DCOLS;
+            for (int g = 0; g < ((TM_DIAG & 4) ? 0 : ng); ++g) {
+              const uint32_t d_tmem = tmem_d0 + dr * DSTRIDE + g * Cfg::DCOLS;
               for (int bb = 0; bb < bpg; ++bb) {
                 const int blob = g * bpg + bb;
                 const uint32_t a_tmem = tmem_a0 + (ac * Cfg::BLOBS + blob) * 32;
@@ -394,9 +428,9 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         }
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp < Cfg::W_SCALE) {
     // ---------------------------------------------------------------- dequant (NDS sets)
-    const int set = (warp - 8) >> 2;  // takes chunks i % NDS == set, TMEM operand slot `set`
+    const int set = warp >> 2;  // takes chunks i % NDS == set, TMEM operand slot `set`
     const int quarter = warp & 3;
     const int row = quarter * 32 + static_cast<int>(lane);
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
@@ -427,7 +461,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         const long long q0 = DCLK();
         mbar_wait(bar_fullw + 8 * ws, (i / NW) & 1);  // the chunk's packed weights landed
         const long long q1 = DCLK();
-        if (i == 0 && warp == 8 && lane == 0) DMARK(2);
+        if (i == 0 && warp == 0 && lane == 0) DMARK(2);
         const uint8_t* wst = w_ptr0 + ws * Cfg::W_BYTES + row * 16;
         uint4 wa = *reinterpret_cast<const uint4*>(wst);
         uint4 wb = *reinterpret_cast<const uint4*>(wst + 2048);
@@ -449,6 +483,10 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
             const int gi = (((kb0 + bb) * 64) >> gshift) - g_base;
             const uint32_t z2 = zero_operand<BF16>(*reinterpret_cast<const uint16_t*>(zs + gi * 256 + row * 2));
             uint32_t rr[32];
+            if (TM_DIAG & 2) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) rr[j] = (j & 1 ? xa.x : xb.y) + j;
+            } else {
             deq_word_int<BF16>(xa.x, z2, rr + 0);
             deq_word_int<BF16>(xa.y, z2, rr + 4);
             deq_word_int<BF16>(xa.z, z2, rr + 8);
@@ -457,6 +495,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
             deq_word_int<BF16>(xb.y, z2, rr + 20);
             deq_word_int<BF16>(xb.z, z2, rr + 24);
             deq_word_int<BF16>(xb.w, z2, rr + 28);
+            }
             tmem_st_32x32b_x32(a_slot + bb * 32, rr);
           }
         }
@@ -466,7 +505,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         mbar_arrive(bar_ready + 8 * r);
         if (lane == 0 && (warp & 3) == 0) DMARK(3);  // last chunk's operands written (latest wins)
         ++mine;
-        if (warp == 8 && lane == 0) {
+        if (warp == 0 && lane == 0) {
           DACC(143, q1 - q0);
           DACC(144, q2 - q1);
           DACC(146, DCLK() - q2);
@@ -475,12 +514,12 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
       }
     }
     if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= Cfg::W_SCALE && warp < Cfg::W_SCALE + 4) {
     // ---------------------------------------------------------------- scale + epilogue
     const int quarter = warp & 3;
     const int row = quarter * 32 + static_cast<int>(lane);
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-    const int et = threadIdx.x - 4 * 32;  // 0..127 (warps 4..7)
+    const int et = threadIdx.x - Cfg::W_SCALE * 32;  // 0..127
     int ci = 0, box = -1;
     DEC_FOR_SEGMENTS {
       const int nt = t % args.n_tiles;
@@ -508,16 +547,33 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         mbar_wait(bar_done + 8 * r, (ci / NR) & 1);
         tc_fence_after();
         const long long q1 = DCLK();
-        for (int g = 0; g < ng; ++g) {
-          const int gi = ((kb0 * 64) >> gshift) + g - g_base;
-          const float sc = __half2float(__ushort_as_half(*reinterpret_cast<const uint16_t*>(ss + gi * 256 + row * 2)));
-#pragma unroll
-          for (int m0 = 0; m0 < NT; m0 += 16) {
-            uint32_t v[16];
-            tmem_ld_32x32b_x16(tmem_d0 + (dr * 4 + g) * Cfg::DCOLS + lane_off + m0, v);
+        const uint32_t d_row = tmem_d0 + dr * DSTRIDE + lane_off;
+        const int gi0 = ((kb0 * 64) >> gshift) - g_base;
+        const auto scale_of = [&](int g) {
+          return __half2float(__ushort_as_half(*reinterpret_cast<const uint16_t*>(ss + (gi0 + g) * 256 + row * 2)));
+        };
+        if (NT <= 32 && (ng * NT) % 32 == 0) {
+          // whole 32-column loads (NT = 16: two groups per load), one wait per load
+          for (int c0 = 0; c0 < ng * NT; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(d_row + c0, v);
+            const float s0 = scale_of(c0 / NT);
+            const float s1 = NT == 16 ? scale_of(c0 / NT + 1) : s0;
             tc_wait_ld();
 #pragma unroll
-            for (int m = 0; m < 16; ++m) acc[m0 + m] = fmaf(sc, __uint_as_float(v[m]), acc[m0 + m]);
+            for (int j = 0; j < 32; ++j) acc[j % NT] = fmaf(j < NT ? s0 : s1, __uint_as_float(v[j]), acc[j % NT]);
+          }
+        } else {
+          for (int g = 0; g < ng; ++g) {
+            const float sc = scale_of(g);
+#pragma unroll
+            for (int m0 = 0; m0 < NT; m0 += 16) {
+              uint32_t v[16];
+              tmem_ld_32x32b_x16(d_row + g * Cfg::DCOLS + m0, v);
+              tc_wait_ld();
+#pragma unroll
+              for (int m = 0; m < 16; ++m) acc[m0 + m] = fmaf(sc, __uint_as_float(v[m]), acc[m0 + m]);
+            }
           }
         }
         tc_fence_before();
@@ -529,58 +585,50 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         ++ci;
       }
       if (et == 0) DMARK(4);  // accumulation of this segment finished (latest segment wins)
-      // ---- segment end: store (whole tile) or stream-K partial + fix-up
+      // ---- segment end.  A CTA's range [u0, u1) meets a shared tile only at its two ends: its
+      // first segment may be the tile's tail (or a middle piece), its last segment the tile's
+      // head.  The tail is computed first in time (start of the contributor's range), the head
+      // last (end of the head holder's range), so the head holder finalises: it waits for the
+      // contributors' flags (long set by then), adds their partials in fixed CTA order
+      // (deterministic) and stores.  A tail only stores its partial and raises its flag.
       const long long tile_lo = static_cast<long long>(t) * kc;
       const long long tile_hi = tile_lo + kc;
-      const bool full = (u == tile_lo) && (cend == tile_hi);
       const int n = nt * 128 + row;
       const int mb = mt * NT;
       const int mcount = (args.M - mb) < NT ? (args.M - mb) : NT;
-      if (full) {
+      if (u != tile_lo) {
+        // tail / middle piece: always this CTA's first segment -> partial slot p, flag p
+        float* ws = args.workspace + static_cast<size_t>(p) * NT * 128;
 #pragma unroll
-        for (int m = 0; m < NT; ++m)
-          if (m < mcount) dec_store<BF16, OUT>(args.out, args.N, mb + m, n, acc[m]);
+        for (int m = 0; m < NT; ++m) __stcg(ws + m * 128 + row, acc[m]);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (et == 0) st_release_gpu(args.counters + p, 1);  // cumulative over the barrier
       } else {
-        const bool is_first_tile = (u == u0);
-        float* ws = args.workspace + (static_cast<size_t>(2 * p + (is_first_tile ? 0 : 1)) * NT) * 128;
-#pragma unroll
-        for (int m = 0; m < NT; ++m) ws[m * 128 + row] = acc[m];
-        __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (et == 0) {
-          const int p_lo = dec_owner(tile_lo, T, P);
+        if (cend != tile_hi) {
+          // head of a shared tile (this CTA's last segment): add the later contributors' partials
           const int p_hi = dec_owner(tile_hi - 1, T, P);
-          const int old = atomicAdd(args.counters + t, 1);
-          const int last = (old == p_hi - p_lo) ? 1 : 0;
-          if (last) args.counters[t] = 0;  // all contributors arrived: ready for the next launch
-          bcast[0] = last;
-          bcast[1] = p_lo;
-          bcast[2] = p_hi;
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        const int last = bcast[0], p_lo = bcast[1], p_hi = bcast[2];
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (last) {
-          __threadfence();
-#pragma unroll
-          for (int m = 0; m < NT; ++m) acc[m] = 0.f;
-          for (int q = p_lo; q <= p_hi; ++q) {  // fixed k order: deterministic
-            const long long qs = dec_start(q, T, P);
-            const int slot = 2 * q + ((qs >= tile_lo) ? 0 : 1);
-            const float* wq = args.workspace + (static_cast<size_t>(slot) * NT) * 128;
+          if (et == 0)
+            for (int q = p + 1; q <= p_hi; ++q)
+              while (ld_acquire_gpu(args.counters + q) == 0) {
+              }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          for (int q = p + 1; q <= p_hi; ++q) {  // fixed k order: deterministic
+            const float* wq = args.workspace + static_cast<size_t>(q) * NT * 128;
 #pragma unroll
             for (int m = 0; m < NT; ++m) acc[m] += __ldcg(wq + m * 128 + row);
           }
-#pragma unroll
-          for (int m = 0; m < NT; ++m)
-            if (m < mcount) dec_store<BF16, OUT>(args.out, args.N, mb + m, n, acc[m]);
+          if (et == 0)
+            for (int q = p + 1; q <= p_hi; ++q) args.counters[q] = 0;  // consumed: zero for the next launch
         }
+#pragma unroll
+        for (int m = 0; m < NT; ++m)
+          if (m < mcount) dec_store<BF16, OUT>(args.out, args.N, mb + m, n, acc[m]);
       }
     }
     if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));
   }
 
-  if (warp == 4 && lane == 0) DMARK(5);  // epilogue finished
+  if (warp == Cfg::W_SCALE && lane == 0) DMARK(5);  // epilogue finished
 #if TM_PROFILE
   if (args.trace) {
     if (threadIdx.x == 0) {
@@ -594,7 +642,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
 #endif
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == Cfg::W_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
