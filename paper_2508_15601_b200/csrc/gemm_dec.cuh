@@ -170,7 +170,7 @@ struct RingPos {
 #define TM_PROFILE 0
 #endif
 // diagnostics only (wrong results): bit 0 no weight loads, bit 1 no dequant math, bit 2 no MMAs,
-// bit 3 no activation loads
+// bit 3 no activation loads, bit 4 no tcgen05.st of operands, bit 5 no tcgen05.ld of D
 #ifndef TM_DIAG
 #define TM_DIAG 0
 #endif
@@ -250,9 +250,12 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
   const int kc = args.kc;
   const int gshift = args.group == 64 ? 6 : 7;
   const int bpg = args.group >> 6;  // blobs per group (1 or 2)
-  const int chunks_per_box = (Cfg::SZG << gshift) / Cfg::CH;
-  const int DR = dec_dring<NT>(args.group);           // D ring entries
-  const int NISSUE = dec_nissue<NT>(DR);
+  const int bshift = gshift - 6;    // log2(bpg)
+  const int box_mask = ((Cfg::SZG << gshift) / Cfg::CH) - 1;  // chunks per s/z box - 1 (2 or 4 chunks)
+  const int DR = dec_dring<NT>(args.group);           // D ring entries (1, 2 or 4)
+  const int dr_mask = DR - 1, dr_shift = DR == 4 ? 2 : DR - 1;
+  const int NISSUE = dec_nissue<NT>(DR);              // 1 or 2
+  const int is_mask = NISSUE - 1;
   const int DSTRIDE = (Cfg::CH >> gshift) * NT;        // D columns per ring entry
 
   if (warp == Cfg::W_PRODW && lane == 0) {
@@ -333,7 +336,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
       const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
       const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
       for (int c = c0; c < c1; ++c, ++i) {
-        if ((c - c0) % chunks_per_box == 0) {  // s/z do not depend on the previous kernel
+        if (((c - c0) & box_mask) == 0) {  // s/z do not depend on the previous kernel
           const int j = box % Cfg::SZ_SLOTS;
           mbar_wait(bar_szempty + 8 * j, ((box / Cfg::SZ_SLOTS) & 1) ^ 1);
           const uint32_t fb = bar_szfull + 8 * j;
@@ -380,28 +383,29 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
     const int me = warp - Cfg::W_MMA;
     constexpr uint32_t idesc = umma_idesc_f16(BF16, 128, NT);
     if (me < NISSUE) {
-      int i = 0;
+      // per-chunk ring positions by counting (no integer division in the loop)
+      int i = 0, ac = 0;
+      RingPos rp;
       DEC_FOR_SEGMENTS {
         const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
         const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
-        for (int c = c0; c < c1; ++c, ++i) {
-          if (i % NISSUE != me) continue;
-          const int r = i % NR;
-          const uint32_t rph = (i / NR) & 1;
-          const int ac = i % NDS;
-          const int dr = i % DR;
+        for (int c = c0; c < c1; ++c, ++i, rp.advance(NR), ac = (ac + 1 == NDS) ? 0 : ac + 1) {
+          if ((i & is_mask) != me) continue;
+          const int r = rp.slot;
+          const uint32_t rph = rp.phase;
+          const int dr = i & dr_mask;
           const int kb0 = c * Cfg::BLOBS;
           const int nb = (KS - kb0) < Cfg::BLOBS ? (KS - kb0) : Cfg::BLOBS;
-          const int ng = nb / bpg;
+          const int ng = nb >> bshift;
           const uint32_t act = a0 + r * Cfg::ACT_BYTES;
           const long long q0 = DCLK();
           mbar_wait(bar_fulla + 8 * r, rph);                    // activations in SMEM
           mbar_wait(bar_ready + 8 * r, rph);                    // operands in TMEM
           const long long q1 = DCLK();
-          mbar_wait(bar_dfree + 8 * dr, ((i / DR) & 1) ^ 1);    // D slots of this ring entry read
+          mbar_wait(bar_dfree + 8 * dr, ((i >> dr_shift) & 1) ^ 1);  // D slots of this ring entry read
           tc_fence_after();
           const long long q2 = DCLK();
-          long long q3 = q2;
+          long long q3 = q2, qf = q2;
           if (elect_one()) {
             for (int g = 0; g < ((TM_DIAG & 4) ? 0 : ng); ++g) {
               const uint32_t d_tmem = tmem_d0 + dr * DSTRIDE + g * Cfg::DCOLS;
@@ -410,8 +414,10 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
                 const uint32_t a_tmem = tmem_a0 + (ac * Cfg::BLOBS + blob) * 32;
                 const uint64_t bdesc0 = umma_desc_sw128(act + blob * (NT * 128));
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
+                for (int j = 0; j < 4; ++j) {
                   mma_ts(d_tmem, a_tmem + 8 * j, bdesc0 + 2 * j, idesc, (bb | j) != 0 ? 1u : 0u);
+                  if (TM_PROFILE && g == 0 && bb == 0 && j == 0) qf = DCLK();
+                }
               }
             }
             q3 = DCLK();
@@ -422,6 +428,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
             DACC(136, q1 - q0);
             DACC(137, q2 - q1);
             DACC(138, q3 - q2);
+            DACC(145, qf - q2);
             DACC(139, DCLK() - q3);
             DACC(140, 1);
           }
@@ -435,41 +442,40 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
     const int row = quarter * 32 + static_cast<int>(lane);
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t a_slot = tmem_a0 + set * Cfg::BLOBS * 32 + lane_off;
-    int i = 0, box = -1, mine = 0;
+    int box = -1, mine = 0, sel = 0;
+    RingPos wp, rp, rp_prev;  // weight ring, ready/done ring, and the set's previous chunk's entry
     bool box_ready = false;
     DEC_FOR_SEGMENTS {
       const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
       const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
       int g_base = 0;
-      for (int c = c0; c < c1; ++c, ++i) {
-        if ((c - c0) % chunks_per_box == 0) {
+      for (int c = c0; c < c1; ++c, wp.advance(NW), rp.advance(NR), sel = (sel + 1 == NDS) ? 0 : sel + 1) {
+        if (((c - c0) & box_mask) == 0) {
           if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));  // leaving box
           ++box;
           box_ready = false;
           g_base = (c * Cfg::CH) >> gshift;
         }
-        if (i % NDS != set) continue;
+        if (sel != set) continue;
         if (!box_ready) {  // wait for the box only before a chunk this set owns
           mbar_wait(bar_szfull + 8 * (box % Cfg::SZ_SLOTS), (box / Cfg::SZ_SLOTS) & 1);
           box_ready = true;
         }
         const uint8_t* zs = sz_ptr0 + (box % Cfg::SZ_SLOTS) * 2 * Cfg::SZ_BOX + Cfg::SZ_BOX;
-        const int r = i % NR;
-        const int ws = i % NW;
+        const int r = rp.slot;
+        const int ws = wp.slot;
         const int kb0 = c * Cfg::BLOBS;
         const int nb = (KS - kb0) < Cfg::BLOBS ? (KS - kb0) : Cfg::BLOBS;
         const long long q0 = DCLK();
-        mbar_wait(bar_fullw + 8 * ws, (i / NW) & 1);  // the chunk's packed weights landed
+        mbar_wait(bar_fullw + 8 * ws, wp.phase);  // the chunk's packed weights landed
         const long long q1 = DCLK();
-        if (i == 0 && warp == 0 && lane == 0) DMARK(2);
+        if (mine == 0 && warp == 0 && lane == 0) DMARK(2);
         const uint8_t* wst = w_ptr0 + ws * Cfg::W_BYTES + row * 16;
         uint4 wa = *reinterpret_cast<const uint4*>(wst);
         uint4 wb = *reinterpret_cast<const uint4*>(wst + 2048);
         // this set's TMEM slot was last read by the MMA of chunk i - NDS
-        if (mine > 0) {
-          const int ip = i - NDS;
-          mbar_wait(bar_done + 8 * (ip % NR), (ip / NR) & 1);
-        }
+        if (mine > 0) mbar_wait(bar_done + 8 * rp_prev.slot, rp_prev.phase);
+        rp_prev = rp;
         tc_fence_after();
         const long long q2 = DCLK();
 #pragma unroll
@@ -496,7 +502,11 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
             deq_word_int<BF16>(xb.z, z2, rr + 24);
             deq_word_int<BF16>(xb.w, z2, rr + 28);
             }
-            tmem_st_32x32b_x32(a_slot + bb * 32, rr);
+            if (TM_DIAG & 16) {
+              keep_alive_32(rr);
+            } else {
+              tmem_st_32x32b_x32(a_slot + bb * 32, rr);
+            }
           }
         }
         mbar_arrive(bar_emptyw + 8 * ws);  // all LDS of the chunk's codes have completed
@@ -521,6 +531,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const int et = threadIdx.x - Cfg::W_SCALE * 32;  // 0..127
     int ci = 0, box = -1;
+    RingPos rps;
     DEC_FOR_SEGMENTS {
       const int nt = t % args.n_tiles;
       const int mt = t / args.n_tiles;
@@ -531,20 +542,22 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
       for (int m = 0; m < NT; ++m) acc[m] = 0.f;
       int g_base = 0;
       for (int c = c0; c < c1; ++c) {
-        if ((c - c0) % chunks_per_box == 0) {
+        const long long qi = DCLK();
+        if (((c - c0) & box_mask) == 0) {
           if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));
           ++box;
           mbar_wait(bar_szfull + 8 * (box % Cfg::SZ_SLOTS), (box / Cfg::SZ_SLOTS) & 1);
           g_base = (c * Cfg::CH) >> gshift;
         }
+        if (et == 0) DACC(155, DCLK() - qi);
         const uint8_t* ss = sz_ptr0 + (box % Cfg::SZ_SLOTS) * 2 * Cfg::SZ_BOX;
         const int kb0 = c * Cfg::BLOBS;
         const int nb = (KS - kb0) < Cfg::BLOBS ? (KS - kb0) : Cfg::BLOBS;
-        const int ng = nb / bpg;
-        const int r = ci % NR;
-        const int dr = ci % DR;
+        const int ng = nb >> bshift;
+        const int r = rps.slot;
+        const int dr = ci & dr_mask;
         const long long q0 = DCLK();
-        mbar_wait(bar_done + 8 * r, (ci / NR) & 1);
+        mbar_wait(bar_done + 8 * r, rps.phase);
         tc_fence_after();
         const long long q1 = DCLK();
         const uint32_t d_row = tmem_d0 + dr * DSTRIDE + lane_off;
@@ -556,7 +569,12 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
           // whole 32-column loads (NT = 16: two groups per load), one wait per load
           for (int c0 = 0; c0 < ng * NT; c0 += 32) {
             uint32_t v[32];
-            tmem_ld_32x32b_x32(d_row + c0, v);
+            if (TM_DIAG & 32) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = 0;
+            } else {
+              tmem_ld_32x32b_x32(d_row + c0, v);
+            }
             const float s0 = scale_of(c0 / NT);
             const float s1 = NT == 16 ? scale_of(c0 / NT + 1) : s0;
             tc_wait_ld();
@@ -581,8 +599,11 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         if (et == 0) {
           DACC(141, q1 - q0);
           DACC(142, DCLK() - q1);
+          DACC(156, DCLK() - qi);
+          DACC(158, 1);
         }
         ++ci;
+        rps.advance(NR);
       }
       if (et == 0) DMARK(4);  // accumulation of this segment finished (latest segment wins)
       // ---- segment end.  A CTA's range [u0, u1) meets a shared tile only at its two ends: its
@@ -591,6 +612,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
       // last (end of the head holder's range), so the head holder finalises: it waits for the
       // contributors' flags (long set by then), adds their partials in fixed CTA order
       // (deterministic) and stores.  A tail only stores its partial and raises its flag.
+      const long long qe = DCLK();
       const long long tile_lo = static_cast<long long>(t) * kc;
       const long long tile_hi = tile_lo + kc;
       const int n = nt * 128 + row;
@@ -624,6 +646,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         for (int m = 0; m < NT; ++m)
           if (m < mcount) dec_store<BF16, OUT>(args.out, args.N, mb + m, n, acc[m]);
       }
+      if (et == 0) DACC(157, DCLK() - qe);
     }
     if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));
   }

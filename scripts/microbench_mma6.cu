@@ -72,6 +72,40 @@ __global__ void __launch_bounds__(512, 1) kern(int chunks, int nbg, unsigned lon
         n += 8;
       }
       if (acc == 0x1234567u) out[300] = acc;
+    } else if (BG == 5 || BG == 6) {
+      const uint32_t z2 = zero_operand<true>(0x4000);
+      const uint32_t taddr = tmem + 256 + ((uint32_t)(q * 32) << 16);
+      uint32_t w = threadIdx.x * 0x9E3779B9u;
+      uint32_t acc = 0;
+      while (!*stop) {
+        uint32_t r[32];
+        if (BG == 5) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = w + j;
+          tmem_st_32x32b_x32(taddr, r);
+          tc_wait_st();
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) deq_word_int<true>(w ^ j, z2, r + 4 * j);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc ^= r[j];
+        }
+        w += 0x1234567u;
+        n += 8;
+      }
+      if (acc == 0x1234567u) out[300] = acc;
+    } else if (BG == 7) {
+      const uint32_t taddr = tmem + 448 + ((uint32_t)(q * 32) << 16);
+      uint32_t acc = 0;
+      while (!*stop) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr, r);
+        tc_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc += r[j];
+        n += 8;
+      }
+      if (acc == 0x1234567u) out[300] = acc;
     } else if (BG == 3) {
       const uint32_t z2 = zero_operand<true>(0x4000);
       const uint32_t taddr = tmem + 256 + ((uint32_t)(q * 32) << 16);  // reads of A use cols 0..383 too; harmless
@@ -101,13 +135,13 @@ template <int BG> void run(int nbg) {
   k<<<148, 512, 128 * 1024>>>(chunks, nbg, d); k<<<148, 512, 128 * 1024>>>(chunks, nbg, d);
   cudaDeviceSynchronize();
   unsigned long long h[400]; cudaMemcpy(h, d, 400 * 8, cudaMemcpyDeviceToHost);
-  const char* names[] = {"idle", "ALU lop3", "LDS.128", "dequant+STTM", "FMA"};
+  const char* names[] = {"idle", "ALU lop3", "LDS.128", "dequant+STTM", "FMA", "STTM only", "dequant only", "LDTM"};
   printf("bg %-13s warps %2d: cycles per chunk %.1f  (bg: %.2f cycles per unit per warp)  %s\n", names[BG], nbg,
          (double)h[0] / chunks, h[148] / 1000.0, cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
 int main() {
   run<0>(0);
-  for (int n : {4, 8, 12}) { run<1>(n); run<2>(n); run<3>(n); run<4>(n); }
+  for (int n : {4, 12}) { run<3>(n); run<5>(n); run<6>(n); run<7>(n); }
   return 0;
 }

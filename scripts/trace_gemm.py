@@ -77,11 +77,15 @@ print("   epi", t[cta, 131:134].tolist())
 if t[:, 140].max() > 0:  # built with TM_PROFILE=1
     n = t[:, 140].astype(float)   # chunks handled by MMA issuer 0
     nd = np.maximum(t[:, 148].astype(float), 1)  # chunks handled by dequant set 0
-    for k, name in {136: "MMA: wait ready", 137: "MMA: wait dfree", 138: "MMA: issue", 139: "MMA: commit+sync"}.items():
+    for k, name in {136: "MMA: wait ready", 137: "MMA: wait dfree", 138: "MMA: issue", 145: "MMA: first MMA issue", 139: "MMA: commit+sync"}.items():
         print(f"per owned chunk {name:22s} {np.median(t[:, k] / n):8.0f} cycles")
     tot = (t[:, 141] + t[:, 142]).astype(float)
     for k, name in {141: "scale: wait done", 142: "scale: work"}.items():
         print(f"per chunk       {name:22s} {np.median(t[:, k] / np.maximum(n * 2, 1)):8.0f} cycles (approx)")
+    ns = np.maximum(t[:, 158].astype(float), 1)
+    for k, name in {155: "scale: box wait", 156: "scale: whole iteration", 141: "scale: wait done (exact)"}.items():
+        print(f"per chunk       {name:22s} {np.median(t[:, k] / ns):8.0f} cycles")
+    print(f"per CTA         scale: segment ends       {np.median(t[:, 157]):8.0f} cycles")
     for k, name in {143: "deq: wait full", 144: "deq: LDS+wait slot", 146: "deq: math+st+arrive"}.items():
         print(f"per owned chunk {name:22s} {np.median(t[:, k] / nd):8.0f} cycles")
     if t[:, 152].max() > 0:
