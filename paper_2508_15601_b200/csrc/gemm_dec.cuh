@@ -38,6 +38,7 @@
 // one commit (MMA), one done wait + one D-slot release (scale).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -170,7 +171,11 @@ struct RingPos {
 #define TM_PROFILE 0
 #endif
 // diagnostics only (wrong results): bit 0 no weight loads, bit 1 no dequant math, bit 2 no MMAs,
-// bit 3 no activation loads, bit 4 no tcgen05.st of operands, bit 5 no tcgen05.ld of D
+// bit 3 no activation loads, bit 4 no tcgen05.st of operands, bit 5 no tcgen05.ld of D,
+// bit 6 tcgen05.st of half the blobs, bit 7 half the MMAs, bit 8 one MMA issuer, bit 9 MMA issuer
+// waits for its chunk's completion, bit 10 MMA issuer skips its waits, bit 11 no fence before the MMAs,
+// bit 12 MMA issuer alone, bit 13 dequant/scale warps skip their tcgen05 fences,
+// bit 14 no scale warps, bit 15 no weight producer / dequant warps
 #ifndef TM_DIAG
 #define TM_DIAG 0
 #endif
@@ -254,7 +259,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
   const int box_mask = ((Cfg::SZG << gshift) / Cfg::CH) - 1;  // chunks per s/z box - 1 (2 or 4 chunks)
   const int DR = dec_dring<NT>(args.group);           // D ring entries (1, 2 or 4)
   const int dr_mask = DR - 1, dr_shift = DR == 4 ? 2 : DR - 1;
-  const int NISSUE = dec_nissue<NT>(DR);              // 1 or 2
+  const int NISSUE = (TM_DIAG & 256) ? 1 : dec_nissue<NT>(DR);  // 1 or 2
   const int is_mask = NISSUE - 1;
   const int DSTRIDE = (Cfg::CH >> gshift) * NT;        // D columns per ring entry
 
@@ -293,7 +298,40 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
   const uint32_t tmem_a0 = tmem_base;                          // NDS x 4 blobs x 32 columns
   const uint32_t tmem_d0 = tmem_base + NDS * Cfg::BLOBS * 32;  // DR x (256 / g) groups x NT columns
 
-  if (warp == Cfg::W_PRODW) {
+  if (TM_DIAG & 4096) {
+    // diagnostic: MMA issuer 0 alone, back-to-back chunks with commit + wait (no other roles)
+    if (warp == Cfg::W_MMA) {
+      constexpr uint32_t idesc = umma_idesc_f16(BF16, 128, NT);
+      const long long q0 = DCLK();
+      const int nchunks = static_cast<int>(u1 - u0);
+      for (int i = 0; i < nchunks; ++i) {
+        const int r = i % NR;
+        if (elect_one()) {
+          for (int g = 0; g < 2; ++g)
+            for (int bb = 0; bb < 2; ++bb) {
+              const int blob = g * 2 + bb;
+              const uint64_t bd = umma_desc_sw128(a0 + r * Cfg::ACT_BYTES + blob * (NT * 128));
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                mma_ts(tmem_d0 + (i & 3) * 32 + g * 16, tmem_a0 + ((i % 3) * 4 + blob) * 32 + 8 * j, bd + 2 * j, idesc,
+                       (bb | j) != 0);
+            }
+          tc_commit(bar_done + 8 * r);
+        }
+        __syncwarp();
+        mbar_wait(bar_done + 8 * r, (i / NR) & 1);
+      }
+      if (lane == 0) {
+        DACC(147, DCLK() - q0);
+        DACC(140, nchunks);
+        DACC(138, 0);
+      }
+    }
+  } else if ((TM_DIAG & 32768) && (warp == Cfg::W_PRODW || warp < Cfg::W_SCALE)) {
+    // diagnostic: no weight producer, no dequant
+  } else if ((TM_DIAG & 16384) && warp >= Cfg::W_SCALE && warp < Cfg::W_SCALE + 4) {
+    // diagnostic: no scale warps
+  } else if (warp == Cfg::W_PRODW) {
     // ---------------------------------------------------------------- producer W
     const uint64_t pol = policy_evict_first();
     RingPos st;
@@ -355,7 +393,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         }
         const long long q0 = DCLK();
         if (i >= NR) {
-          mbar_wait(bar_done + 8 * prev.slot, prev.phase);  // MMA of chunk i - NR read the slot
+          if (!(TM_DIAG & 1024)) mbar_wait(bar_done + 8 * prev.slot, prev.phase);  // MMA of chunk i - NR read the slot
           prev.advance(NR);
         }
         const long long q1 = DCLK();
@@ -399,24 +437,46 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
           const int ng = nb >> bshift;
           const uint32_t act = a0 + r * Cfg::ACT_BYTES;
           const long long q0 = DCLK();
-          mbar_wait(bar_fulla + 8 * r, rph);                    // activations in SMEM
-          mbar_wait(bar_ready + 8 * r, rph);                    // operands in TMEM
+          if (!(TM_DIAG & 1024)) {
+            mbar_wait(bar_fulla + 8 * r, rph);                    // activations in SMEM
+            if (!(TM_DIAG & 32768)) mbar_wait(bar_ready + 8 * r, rph);  // operands in TMEM
+          }
           const long long q1 = DCLK();
-          mbar_wait(bar_dfree + 8 * dr, ((i >> dr_shift) & 1) ^ 1);  // D slots of this ring entry read
-          tc_fence_after();
+          if (!(TM_DIAG & (1024 | 16384))) mbar_wait(bar_dfree + 8 * dr, ((i >> dr_shift) & 1) ^ 1);  // D slots read
+          if (!(TM_DIAG & 2048)) tc_fence_after();
           const long long q2 = DCLK();
           long long q3 = q2, qf = q2;
           if (elect_one()) {
-            for (int g = 0; g < ((TM_DIAG & 4) ? 0 : ng); ++g) {
-              const uint32_t d_tmem = tmem_d0 + dr * DSTRIDE + g * Cfg::DCOLS;
-              for (int bb = 0; bb < bpg; ++bb) {
-                const int blob = g * bpg + bb;
-                const uint32_t a_tmem = tmem_a0 + (ac * Cfg::BLOBS + blob) * 32;
-                const uint64_t bdesc0 = umma_desc_sw128(act + blob * (NT * 128));
+            const uint32_t d_base = tmem_d0 + dr * DSTRIDE;
+            const uint32_t a_base = tmem_a0 + ac * Cfg::BLOBS * 32;
+            // full chunk: 16 MMAs with compile-time operand offsets (no loop-carried address math)
+            const auto issue_full = [&](auto bpg_c) {
+              constexpr int BPG = decltype(bpg_c)::value;
+              const uint64_t bdesc = umma_desc_sw128(act);
+#pragma unroll
+              for (int blob = 0; blob < Cfg::BLOBS; ++blob)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                  mma_ts(d_tmem, a_tmem + 8 * j, bdesc0 + 2 * j, idesc, (bb | j) != 0 ? 1u : 0u);
-                  if (TM_PROFILE && g == 0 && bb == 0 && j == 0) qf = DCLK();
+                  if ((TM_DIAG & 128) && (j & 1)) continue;
+                  mma_ts(d_base + (blob / BPG) * Cfg::DCOLS, a_base + blob * 32 + 8 * j,
+                         bdesc + ((blob * NT * 128) >> 4) + 2 * j, idesc, ((blob % BPG) | j) != 0 ? 1u : 0u);
+                  if (TM_PROFILE && blob == 0 && j == 0) qf = DCLK();
+                }
+            };
+            if (TM_DIAG & 4) {
+            } else if (nb == Cfg::BLOBS && bpg == 2) {
+              issue_full(std::integral_constant<int, 2>{});
+            } else if (nb == Cfg::BLOBS) {
+              issue_full(std::integral_constant<int, 1>{});
+            } else {
+              for (int g = 0; g < ng; ++g) {  // K tail: partial chunk
+                for (int bb = 0; bb < bpg; ++bb) {
+                  const int blob = g * bpg + bb;
+                  const uint64_t bdesc0 = umma_desc_sw128(act + blob * (NT * 128));
+#pragma unroll
+                  for (int j = 0; j < 4; ++j)
+                    mma_ts(d_base + g * Cfg::DCOLS, a_base + blob * 32 + 8 * j, bdesc0 + 2 * j, idesc,
+                           (bb | j) != 0 ? 1u : 0u);
                 }
               }
             }
@@ -424,6 +484,10 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
             tc_commit(bar_done + 8 * r);
           }
           __syncwarp();
+          if (TM_DIAG & 512) {  // MMA completion latency (diagnostic: serialises chunks)
+            mbar_wait(bar_done + 8 * r, rph);
+            if (me == 0 && lane == 0) DACC(147, DCLK() - q2);
+          }
           if (me == 0 && lane == 0) {
             DACC(136, q1 - q0);
             DACC(137, q2 - q1);
@@ -474,9 +538,9 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         uint4 wa = *reinterpret_cast<const uint4*>(wst);
         uint4 wb = *reinterpret_cast<const uint4*>(wst + 2048);
         // this set's TMEM slot was last read by the MMA of chunk i - NDS
-        if (mine > 0) mbar_wait(bar_done + 8 * rp_prev.slot, rp_prev.phase);
+        if (mine > 0 && !(TM_DIAG & 1024)) mbar_wait(bar_done + 8 * rp_prev.slot, rp_prev.phase);
         rp_prev = rp;
-        tc_fence_after();
+        if (!(TM_DIAG & 8192)) tc_fence_after();
         const long long q2 = DCLK();
 #pragma unroll
         for (int bb = 0; bb < 4; ++bb) {
@@ -502,7 +566,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
             deq_word_int<BF16>(xb.z, z2, rr + 24);
             deq_word_int<BF16>(xb.w, z2, rr + 28);
             }
-            if (TM_DIAG & 16) {
+            if ((TM_DIAG & 16) || ((TM_DIAG & 64) && bb >= 2)) {
               keep_alive_32(rr);
             } else {
               tmem_st_32x32b_x32(a_slot + bb * 32, rr);
@@ -510,8 +574,8 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
           }
         }
         mbar_arrive(bar_emptyw + 8 * ws);  // all LDS of the chunk's codes have completed
-        tc_wait_st();
-        tc_fence_before();
+        if (!(TM_DIAG & 8192)) tc_wait_st();
+        if (!(TM_DIAG & 8192)) tc_fence_before();
         mbar_arrive(bar_ready + 8 * r);
         if (lane == 0 && (warp & 3) == 0) DMARK(3);  // last chunk's operands written (latest wins)
         ++mine;
@@ -557,8 +621,8 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         const int r = rps.slot;
         const int dr = ci & dr_mask;
         const long long q0 = DCLK();
-        mbar_wait(bar_done + 8 * r, rps.phase);
-        tc_fence_after();
+        if (!(TM_DIAG & 1024)) mbar_wait(bar_done + 8 * r, rps.phase);
+        if (!(TM_DIAG & 8192)) tc_fence_after();
         const long long q1 = DCLK();
         const uint32_t d_row = tmem_d0 + dr * DSTRIDE + lane_off;
         const int gi0 = ((kb0 * 64) >> gshift) - g_base;
@@ -594,7 +658,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
             }
           }
         }
-        tc_fence_before();
+        if (!(TM_DIAG & 8192)) tc_fence_before();
         mbar_arrive(bar_dfree + 8 * dr);
         if (et == 0) {
           DACC(141, q1 - q0);
@@ -631,8 +695,8 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
           const int p_hi = dec_owner(tile_hi - 1, T, P);
           if (et == 0)
             for (int q = p + 1; q <= p_hi; ++q)
-              while (ld_acquire_gpu(args.counters + q) == 0) {
-              }
+              for (uint32_t spins = 0; ld_acquire_gpu(args.counters + q) == 0;)
+                if (++spins == (1u << 24)) __trap();  // a contributor never arrived: fail, do not hang
           asm volatile("bar.sync 1, 128;" ::: "memory");
           for (int q = p + 1; q <= p_hi; ++q) {  // fixed k order: deterministic
             const float* wq = args.workspace + static_cast<size_t>(q) * NT * 128;

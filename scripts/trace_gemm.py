@@ -77,7 +77,7 @@ print("   epi", t[cta, 131:134].tolist())
 if t[:, 140].max() > 0:  # built with TM_PROFILE=1
     n = t[:, 140].astype(float)   # chunks handled by MMA issuer 0
     nd = np.maximum(t[:, 148].astype(float), 1)  # chunks handled by dequant set 0
-    for k, name in {136: "MMA: wait ready", 137: "MMA: wait dfree", 138: "MMA: issue", 145: "MMA: first MMA issue", 139: "MMA: commit+sync"}.items():
+    for k, name in {136: "MMA: wait ready", 137: "MMA: wait dfree", 138: "MMA: issue", 145: "MMA: first MMA issue", 147: "MMA: fence->complete", 139: "MMA: commit+sync"}.items():
         print(f"per owned chunk {name:22s} {np.median(t[:, k] / n):8.0f} cycles")
     tot = (t[:, 141] + t[:, 142]).astype(float)
     for k, name in {141: "scale: wait done", 142: "scale: work"}.items():
