@@ -535,28 +535,25 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         const long long q1 = DCLK();
         if (mine == 0 && warp == 0 && lane == 0) DMARK(2);
         const uint8_t* wst = w_ptr0 + ws * Cfg::W_BYTES + row * 16;
-        uint4 wa = *reinterpret_cast<const uint4*>(wst);
-        uint4 wb = *reinterpret_cast<const uint4*>(wst + 2048);
+        // zero operands of the chunk's groups (g = 128: 2, g = 64: 4), before the slot wait
+        const int gi0 = ((kb0 * 64) >> gshift) - g_base;
+        const auto zop = [&](int g) {
+          return zero_operand<BF16>(*reinterpret_cast<const uint16_t*>(zs + (gi0 + g) * 256 + row * 2));
+        };
         // this set's TMEM slot was last read by the MMA of chunk i - NDS
         if (mine > 0 && !(TM_DIAG & 1024)) mbar_wait(bar_done + 8 * rp_prev.slot, rp_prev.phase);
         rp_prev = rp;
         if (!(TM_DIAG & 8192)) tc_fence_after();
         const long long q2 = DCLK();
+        // one blob: 8 LAYOUT v1 words (two LDS.128) -> 32 operand registers -> tcgen05.st x32
+        const auto blob_to_tmem = [&](int bb, uint32_t z2) {
+          const uint4 xa = *reinterpret_cast<const uint4*>(wst + bb * 4096);
+          const uint4 xb = *reinterpret_cast<const uint4*>(wst + bb * 4096 + 2048);
+          uint32_t rr[32];
+          if (TM_DIAG & 2) {
 #pragma unroll
-        for (int bb = 0; bb < 4; ++bb) {
-          if (bb < nb) {
-            const uint4 xa = wa, xb = wb;
-            if (bb + 1 < nb) {
-              wa = *reinterpret_cast<const uint4*>(wst + (bb + 1) * 4096);
-              wb = *reinterpret_cast<const uint4*>(wst + (bb + 1) * 4096 + 2048);
-            }
-            const int gi = (((kb0 + bb) * 64) >> gshift) - g_base;
-            const uint32_t z2 = zero_operand<BF16>(*reinterpret_cast<const uint16_t*>(zs + gi * 256 + row * 2));
-            uint32_t rr[32];
-            if (TM_DIAG & 2) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) rr[j] = (j & 1 ? xa.x : xb.y) + j;
-            } else {
+            for (int j = 0; j < 32; ++j) rr[j] = (j & 1 ? xa.x : xb.y) + j;
+          } else {
             deq_word_int<BF16>(xa.x, z2, rr + 0);
             deq_word_int<BF16>(xa.y, z2, rr + 4);
             deq_word_int<BF16>(xa.z, z2, rr + 8);
@@ -565,16 +562,30 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
             deq_word_int<BF16>(xb.y, z2, rr + 20);
             deq_word_int<BF16>(xb.z, z2, rr + 24);
             deq_word_int<BF16>(xb.w, z2, rr + 28);
-            }
-            if ((TM_DIAG & 16) || ((TM_DIAG & 64) && bb >= 2)) {
-              keep_alive_32(rr);
-            } else {
-              tmem_st_32x32b_x32(a_slot + bb * 32, rr);
-            }
           }
+          if ((TM_DIAG & 16) || ((TM_DIAG & 64) && bb >= 2))
+            keep_alive_32(rr);
+          else
+            tmem_st_32x32b_x32(a_slot + bb * 32, rr);
+        };
+        if (nb == Cfg::BLOBS && bpg == 2) {  // full chunk, g = 128 (straight-line)
+          const uint32_t z0 = zop(0), z1 = zop(1);
+          blob_to_tmem(0, z0);
+          blob_to_tmem(1, z0);
+          blob_to_tmem(2, z1);
+          blob_to_tmem(3, z1);
+        } else if (nb == Cfg::BLOBS) {      // full chunk, g = 64
+          blob_to_tmem(0, zop(0));
+          blob_to_tmem(1, zop(1));
+          blob_to_tmem(2, zop(2));
+          blob_to_tmem(3, zop(3));
+        } else {                            // K tail
+          for (int bb = 0; bb < nb; ++bb) blob_to_tmem(bb, zop(bb >> bshift));
         }
+        const long long q3 = DCLK();
         mbar_arrive(bar_emptyw + 8 * ws);  // all LDS of the chunk's codes have completed
         if (!(TM_DIAG & 8192)) tc_wait_st();
+        const long long q4 = DCLK();
         if (!(TM_DIAG & 8192)) tc_fence_before();
         mbar_arrive(bar_ready + 8 * r);
         if (lane == 0 && (warp & 3) == 0) DMARK(3);  // last chunk's operands written (latest wins)
@@ -584,6 +595,8 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
           DACC(144, q2 - q1);
           DACC(146, DCLK() - q2);
           DACC(148, 1);
+          DACC(159, q3 - q2);
+          DACC(149, q4 - q3);
         }
       }
     }

@@ -86,7 +86,7 @@ if t[:, 140].max() > 0:  # built with TM_PROFILE=1
     for k, name in {155: "scale: box wait", 156: "scale: whole iteration", 141: "scale: wait done (exact)"}.items():
         print(f"per chunk       {name:22s} {np.median(t[:, k] / ns):8.0f} cycles")
     print(f"per CTA         scale: segment ends       {np.median(t[:, 157]):8.0f} cycles")
-    for k, name in {143: "deq: wait full", 144: "deq: LDS+wait slot", 146: "deq: math+st+arrive"}.items():
+    for k, name in {143: "deq: wait full", 144: "deq: LDS+wait slot", 146: "deq: math+st+arrive", 159: "deq: math+st issue", 149: "deq: wait st"}.items():
         print(f"per owned chunk {name:22s} {np.median(t[:, k] / nd):8.0f} cycles")
     if t[:, 152].max() > 0:
         npc = t[:, 152].astype(float)
