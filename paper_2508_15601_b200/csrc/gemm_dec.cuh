@@ -67,8 +67,8 @@ struct DecCfg {
   static constexpr int BLOBS = 4;                        // LAYOUT v1 blobs per chunk
   static constexpr int ACT_BYTES = NT * CH * 2;          // activation chunk (4 SW128 sub-tiles)
   static constexpr int W_BYTES = BLOBS * 4096;           // packed weight chunk
-  static constexpr int NW = NT <= 16 ? 8 : (NT <= 32 ? 6 : 5);  // weight ring (freed after the dequant's LDS)
-  static constexpr int NA = NT <= 32 ? 6 : 3;            // activation ring = per-chunk ready/done ring
+  static constexpr int NW = NT <= 16 ? 8 : (NT <= 32 ? 6 : 5);   // weight ring (freed after the dequant's LDS)
+  static constexpr int NA = NT <= 32 ? 6 : 4;            // activation ring = per-chunk ready/done ring
   static constexpr int NDS = NT <= 16 ? 3 : 2;           // dequant sets = TMEM operand slots
   static constexpr int DCOLS = NT;                       // one D_g slot
   static constexpr int DAVAIL = 512 - NDS * BLOBS * 32;  // TMEM columns left for the D ring
@@ -90,7 +90,10 @@ struct DecCfg {
   static constexpr int HDR = 1024;
   static constexpr int SMEM = 1024 + HDR + NW * W_BYTES + NA * ACT_BYTES + SZ_SLOTS * 2 * SZ_BOX;
   static_assert(DAVAIL >= 4 * NT, "TMEM: one chunk of g = 64 D slots");
-  static_assert(NA >= NDS, "rings");
+  // a ready/done ring entry must be reused by the same dequant set (NA % NDS == 0: that set's
+  // previous use is gated by the MMA completion it waits for) -- measured: NA = 4 with 3 sets
+  // let a set arrive on an entry whose previous phase the MMA had not yet consumed
+  static_assert(NA >= NDS && NA % NDS == 0, "rings");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
