@@ -95,6 +95,9 @@ struct DecCfg {
   // let a set arrive on an entry whose previous phase the MMA had not yet consumed
   static_assert(NA >= NDS && NA % NDS == 0, "rings");
   static_assert(SMEM <= 227 * 1024, "shared memory");
+  // barrier block [fullw NW][emptyw NW][fulla NA][ready NA][done NA][dfree DR_MAX][szfull][szempty]
+  // (+ TMEM slot word) fits the header
+  static_assert((2 * NW + 3 * NA + DR_MAX + 2 * SZ_SLOTS) * 8 + 64 <= HDR, "barrier header");
 };
 
 // D ring depth for this launch: a chunk's D slots take (256 / group) * NT columns, so g = 128
@@ -266,25 +269,67 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
   const int is_mask = NISSUE - 1;
   const int DSTRIDE = (Cfg::CH >> gshift) * NT;        // D columns per ring entry
 
-  if (warp == Cfg::W_PRODW && lane == 0) {
-    prefetch_tmap(&tmap_a);
-    prefetch_tmap(&tmap_s);
-    prefetch_tmap(&tmap_z);
-    for (int w = 0; w < NW; ++w) {
-      mbar_init(bar_fullw + 8 * w, 1);
-      mbar_init(bar_emptyw + 8 * w, 128);
+  // ---- weight producer: one lane per barrier initialises them (the mbarriers are contiguous
+  // from bar_fullw); produce_w issues the weight chunks of this CTA's range
+  const uint64_t w_policy = policy_evict_first();
+  RingPos w_st;
+  int w_i = 0;
+  const auto produce_w = [&](int i_end) {  // weight chunks [w_i, i_end) of this CTA's range
+    int i = 0;
+    DEC_FOR_SEGMENTS {
+      const int nt = t % args.n_tiles;
+      const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
+      const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
+      for (int c = c0; c < c1; ++c, ++i) {
+        if (i < w_i) continue;
+        if (i >= i_end) return;
+        const long long q0 = DCLK();
+        mbar_wait(bar_emptyw + 8 * w_st.slot, w_st.phase ^ 1u);  // the dequant of chunk i - NW read it
+        const long long q1 = DCLK();
+        const int kb0 = c * Cfg::BLOBS;
+        const int nb = (KS - kb0) < Cfg::BLOBS ? (KS - kb0) : Cfg::BLOBS;
+        const uint32_t fb = bar_fullw + 8 * w_st.slot;
+        if (TM_DIAG & 1) {
+          if (elect_one()) mbar_arrive(fb);
+        } else if (elect_one()) {
+          mbar_arrive_expect_tx(fb, nb * 4096);
+          bulk_g2s_hint(w0 + w_st.slot * Cfg::W_BYTES, args.packed + (static_cast<size_t>(nt) * KS + kb0) * 4096,
+                        nb * 4096, fb, w_policy);
+        }
+        __syncwarp();
+        w_st.advance(NW);
+        w_i = i + 1;
+        if (lane == 0) {
+          DACC(150, q1 - q0);
+          DACC(151, DCLK() - q1);
+          DACC(152, 1);
+        }
+      }
     }
-    for (int r = 0; r < NR; ++r) {
-      mbar_init(bar_fulla + 8 * r, 1);
-      mbar_init(bar_ready + 8 * r, 128);
-      mbar_init(bar_done + 8 * r, 1);
-    }
-    for (int d = 0; d < DR_MAX; ++d) mbar_init(bar_dfree + 8 * d, 128);
-    for (int j = 0; j < Cfg::SZ_SLOTS; ++j) {
-      mbar_init(bar_szfull + 8 * j, 1);
-      mbar_init(bar_szempty + 8 * j, 128 * NDS + 128);
+  };
+  if (warp == Cfg::W_PRODW) {
+    constexpr int NBAR = 2 * NW + 3 * NR + DR_MAX + 2 * Cfg::SZ_SLOTS;
+    for (int b = static_cast<int>(lane); b < NBAR; b += 32) {
+      uint32_t cnt;
+      if (b < NW) cnt = 1;                                   // fullw
+      else if (b < 2 * NW) cnt = 128;                        // emptyw
+      else if (b < 2 * NW + NR) cnt = 1;                     // fulla
+      else if (b < 2 * NW + 2 * NR) cnt = 128;               // ready
+      else if (b < 2 * NW + 3 * NR) cnt = 1;                 // done
+      else if (b < 2 * NW + 3 * NR + DR_MAX) cnt = 128;      // dfree
+      else if (b < NBAR - Cfg::SZ_SLOTS) cnt = 1;            // szfull
+      else cnt = 128 * NDS + 128;                            // szempty
+      mbar_init(bar_fullw + 8 * b, cnt);
     }
     fence_mbar_init();
+    __syncwarp();
+    if (lane == 0) {
+      prefetch_tmap(&tmap_a);
+      prefetch_tmap(&tmap_s);
+      prefetch_tmap(&tmap_z);
+    }
+    // (requesting the first chunks here was measured slower: the setup grew by ~1500 cycles
+    // and the first chunk still landed ~5900 cycles after the CTA start -- HBM latency)
   }
   if (warp == Cfg::W_MMA) {
     tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
@@ -335,37 +380,8 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
   } else if ((TM_DIAG & 16384) && warp >= Cfg::W_SCALE && warp < Cfg::W_SCALE + 4) {
     // diagnostic: no scale warps
   } else if (warp == Cfg::W_PRODW) {
-    // ---------------------------------------------------------------- producer W
-    const uint64_t pol = policy_evict_first();
-    RingPos st;
-    int i = 0;
-    DEC_FOR_SEGMENTS {
-      const int nt = t % args.n_tiles;
-      const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
-      const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
-      for (int c = c0; c < c1; ++c, ++i) {
-        const long long q0 = DCLK();
-        mbar_wait(bar_emptyw + 8 * st.slot, st.phase ^ 1u);  // the dequant of chunk i - NW read it
-        const long long q1 = DCLK();
-        const int kb0 = c * Cfg::BLOBS;
-        const int nb = (KS - kb0) < Cfg::BLOBS ? (KS - kb0) : Cfg::BLOBS;
-        const uint32_t fb = bar_fullw + 8 * st.slot;
-        if (TM_DIAG & 1) {
-          if (elect_one()) mbar_arrive(fb);
-        } else if (elect_one()) {
-          mbar_arrive_expect_tx(fb, nb * 4096);
-          bulk_g2s_hint(w0 + st.slot * Cfg::W_BYTES, args.packed + (static_cast<size_t>(nt) * KS + kb0) * 4096,
-                        nb * 4096, fb, pol);
-        }
-        __syncwarp();
-        st.advance(NW);
-        if (lane == 0) {
-          DACC(150, q1 - q0);
-          DACC(151, DCLK() - q1);
-          DACC(152, 1);
-        }
-      }
-    }
+    // ---------------------------------------------------------------- producer W (the rest)
+    produce_w(1 << 30);
   } else if (warp == Cfg::W_PRODA) {
     // ---------------------------------------------------------------- producer A (+ s/z boxes)
     RingPos st, prev;
