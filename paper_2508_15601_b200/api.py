@@ -12,7 +12,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtm_w4a16.so")
+# TM_LIB_PATH: an alternative build of the same library (A/B timing scripts); default in-tree
+LIB_PATH = os.environ.get("TM_LIB_PATH") or os.path.join(_HERE, "libtm_w4a16.so")
 
 TM_LAYOUT_V1 = 1
 
@@ -47,6 +48,8 @@ _SIGS = {
     "tm_dequant_w4": (_I, [ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _P]),
     "tm_set_gemm_override": (_I, [_I, _I]),
     "tm_query_gemm_config": (_I, [_I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I)]),
+    "tm_query_gemm_kind": (_I, [_I, _I, _I, ctypes.POINTER(_I)]),
+    "tm_set_decode_cluster": (_I, [_I]),
     "tm_set_trace": (_I, [_P, ctypes.c_int64]),
     "tm_status_string": (ctypes.c_char_p, [_I]),
     "tm_version": (ctypes.c_char_p, []),
@@ -62,7 +65,12 @@ def lib():
                           "(no fallback path exists)")
         handle = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
-            fn = getattr(handle, name)
+            try:
+                fn = getattr(handle, name)
+            except AttributeError:
+                if LIB_PATH.endswith(os.path.join("paper_2508_15601_b200", "libtm_w4a16.so")):
+                    raise  # the in-tree build must export the whole header
+                continue  # an older build under TM_LIB_PATH (A/B timing): calls to it fail later
             fn.restype = res
             fn.argtypes = args
         _lib = handle
@@ -175,9 +183,15 @@ def set_gemm_override(tile_m=0, split_k=0):
 
 
 def query_gemm_config(M, N, K):
-    t, s, g = _I(), _I(), _I()
+    t, s, g, k = _I(), _I(), _I(), _I()
     _check(lib().tm_query_gemm_config(M, N, K, ctypes.byref(t), ctypes.byref(s), ctypes.byref(g)))
-    return dict(tile_m=t.value, split_k=s.value, grid_ctas=g.value)
+    _check(lib().tm_query_gemm_kind(M, N, K, ctypes.byref(k)))
+    return dict(tile_m=t.value, split_k=s.value, grid_ctas=g.value, kind=k.value)
+
+
+def set_decode_cluster(cs=0):
+    """Tests/benchmarks: 0 automatic, 1 never (stream-K), 2..8 forced CTAs per tile."""
+    _check(lib().tm_set_decode_cluster(cs))
 
 
 def set_trace(buf=None):

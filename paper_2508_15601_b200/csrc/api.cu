@@ -24,6 +24,7 @@ constexpr int kNumSMsDefault = 148;
 
 std::atomic<int> g_override_tile{0};
 std::atomic<int> g_override_split{0};
+std::atomic<int> g_dec_cluster{0};  // 0 automatic, 1 never (stream-K), 2..8 forced size
 uint32_t* g_trace = nullptr;  // debug timeline buffer (tm_set_trace)
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -217,7 +218,8 @@ tm_status get_workspace(cudaStream_t stream, size_t partial_bytes, int n_counter
 
 // ---------------------------------------------------------------- launch configuration
 struct Config {
-  int kind;  // 0 = classic tiles (+ cluster split-K), 1 = persistent stream-K
+  int kind;  // 0 = classic tiles (+ cluster split-K), 1 = persistent stream-K, 2 = decode kernel
+             // with CS CTAs per tile reduced over a thread-block cluster (split = CS)
   int NT;
   int split;  // classic: CTAs per tile along K; stream-K: number of persistent CTAs
   int grid_x, grid_y;
@@ -233,6 +235,56 @@ int max_split_for(int nt) {
     case 128: return GemmCfg<128>::MAX_SPLIT;
     default: return GemmCfg<256>::MAX_SPLIT;
   }
+}
+
+// how many clusters of `cs` decode CTAs can be resident at once (one wave); cached per (nt, cs)
+template <int NT>
+int dec_active_clusters_t(int cs) {
+  static std::atomic<int> cache[9] = {};
+  int v = cache[cs].load();
+  if (v) return v;
+  auto kern = w4a16_dec_kernel<NT, true, OUT_ACT>;
+  const int fallback = num_sms() / cs;  // no device (host-side query): ideal packing
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DecCfg<NT>::SMEM) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fallback > 0 ? fallback : 1;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cs * 64, 1, 1);
+  cfg.blockDim = dim3(DecCfg<NT>::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = DecCfg<NT>::SMEM;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    (void)cudaGetLastError();
+    n = fallback;
+  }
+  if (n < 1) n = 1;
+  cache[cs].store(n);
+  return n;
+}
+int dec_active_clusters(int nt, int cs) {
+  switch (nt) {
+    case 16: return dec_active_clusters_t<16>(cs);
+    case 32: return dec_active_clusters_t<32>(cs);
+    case 64: return dec_active_clusters_t<64>(cs);
+  }
+  return 0;
+}
+
+int dec_max_cluster(int nt) {
+  switch (nt) {
+    case 16: return DecCfg<16>::MAX_CLUSTER;
+    case 32: return DecCfg<32>::MAX_CLUSTER;
+    case 64: return DecCfg<64>::MAX_CLUSTER;
+  }
+  return 1;
 }
 
 Config choose_config(int M, int N, int K) {
@@ -258,6 +310,36 @@ Config choose_config(int M, int N, int K) {
   const int KS = K / 64;
   int split = 1;
   const int os = g_override_split.load();
+  if (os == 0 && nt <= 64) {
+    // decode: a few tiles (o/qkv/down-sized N) -> CS CTAs per tile in one cluster, reduced in
+    // distributed shared memory (no global flags, no gpu-scope fences); else stream-K
+    // (measured on Llama-3-8B decode shapes: fixed per-CTA costs make ~8+ chunks of 256 k per
+    // CTA the sweet spot -- o_proj 64 CTAs 6.6 us vs 128 CTAs 7.0 us vs stream-K 8.1 us -- and a
+    // cluster layout that does not fit one wave is ~1.5x slower)
+    const int tiles = n_tiles * m_tiles;
+    const int kc = (K + 255) / 256;
+    const int force = g_dec_cluster.load();
+    const int cmax = dec_max_cluster(nt);
+    int cs = 0;
+    if (force >= 2) {
+      cs = force < cmax ? force : cmax;
+      if (cs > kc) cs = kc;
+    } else if (force == 0) {
+      for (int k = cmax; k >= 2; --k) {
+        if (k > kc || (kc + k - 1) / k < 8 || tiles * k > num_sms()) continue;
+        if (tiles > dec_active_clusters(nt, k)) continue;
+        cs = k;
+        break;
+      }
+    }
+    if (cs >= 2) {
+      c.kind = 2;
+      c.split = cs;
+      c.grid_x = tiles * cs;
+      c.grid_y = 1;
+      return c;
+    }
+  }
   if (os < 0 || (os == 0 && nt <= 64)) {
     // persistent stream-K: one CTA per SM (or -os CTAs when forced), equal chunk ranges
     c.kind = 1;
@@ -415,20 +497,29 @@ tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaSt
   a.kc = (g.K + Cfg::CH - 1) / Cfg::CH;
   a.total = static_cast<long long>(a.m_tiles) * a.n_tiles * a.kc;
   a.trace = g_trace;
+  a.cluster = c.kind == 2 ? c.split : 0;
+  if (a.total * static_cast<long long>(c.split) >= (1ll << 32)) return TM_ERR_UNSUPPORTED_SHAPE;  // 32-bit range math
   // one partial slot and one flag per CTA (its first segment)
   st = get_workspace(stream, static_cast<size_t>(c.split) * NT * 128 * sizeof(float), c.split, &a.counters,
                      &a.workspace);
   if (st != TM_OK) return st;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(c.split, 1, 1);
+  cfg.gridDim = dim3(c.kind == 2 ? c.grid_x : c.split, 1, 1);
   cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = stream;
-  cudaLaunchAttribute attrs[1];
+  cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attrs[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
+  if (c.kind == 2 && c.split > 1) {
+    attrs[1].id = cudaLaunchAttributeClusterDimension;
+    attrs[1].val.clusterDim.x = c.split;
+    attrs[1].val.clusterDim.y = 1;
+    attrs[1].val.clusterDim.z = 1;
+    cfg.numAttrs = 2;
+  }
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, ms, mz, a);
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
@@ -486,7 +577,7 @@ tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* sca
   args.split = c.split;
   args.trace = g_trace;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (c.kind == 1) {
+  if (c.kind == 1 || c.kind == 2) {
     if (out_kind == OUT_F32) return launch_sk<true, OUT_F32>(A, args, c, s);
     return bf16 ? launch_sk<true, OUT_ACT>(A, args, c, s) : launch_sk<false, OUT_ACT>(A, args, c, s);
   }
@@ -613,6 +704,18 @@ tm_status tm_query_gemm_config(int M, int N, int K, int* tile_m, int* split_k, i
   if (split_k) *split_k = c.split;
   if (grid_ctas) *grid_ctas = c.grid_x * c.grid_y;
   if (split_k && c.kind == 1) *split_k = -c.split;  // negative: persistent stream-K CTA count
+  return TM_OK;
+}
+
+tm_status tm_query_gemm_kind(int M, int N, int K, int* kind) {
+  if (M <= 0 || N <= 0 || K <= 0 || N % 128 || K % 64 || !kind) return TM_ERR_INVALID_ARG;
+  *kind = choose_config(M, N, K).kind;
+  return TM_OK;
+}
+
+tm_status tm_set_decode_cluster(int cs) {
+  if (cs < 0 || cs > 8) return TM_ERR_INVALID_ARG;
+  g_dec_cluster.store(cs);
   return TM_OK;
 }
 

@@ -58,6 +58,8 @@ struct DecArgs {
   int n_tiles, m_tiles;
   int kc;                 // chunks per tile = ceil(K / 256)
   long long total;        // m_tiles * n_tiles * kc
+  int cluster;            // 0: persistent stream-K over [0, total); CS >= 1: CS CTAs per tile
+                          // (a thread-block cluster when CS > 1), tile = blockIdx.x / CS
   uint32_t* trace;
 };
 
@@ -74,19 +76,21 @@ struct DecCfg {
   static constexpr int DAVAIL = 512 - NDS * BLOBS * 32;  // TMEM columns left for the D ring
   static constexpr int DR_MAX = 4;                       // D ring entries (chunks); runtime: dec_dring()
   static constexpr int THREADS = 32 * (8 + 4 * NDS);     // a multiple of 4 warps (per-SMSP registers)
-  // warp roles, ordered by issue priority: the SM's warp arbiter picks the highest eligible warp
-  // id first, so the latency-critical single-thread roles get the highest ids and the ALU-bound
-  // dequant warps the lowest (measured: with the producers/MMA at ids 0-3 the MMA issuer was
-  // starved to ~47 cycles per MMA; ~20 in isolation)
-  static constexpr int W_DEQ = 0;                        // 4 * NDS dequant warps
-  static constexpr int W_SCALE = 4 * NDS;                // 4 scale / epilogue warps
-  static constexpr int W_MMA = 4 * NDS + 4;              // 2 MMA issuer warps (also TMEM allocator)
-  static constexpr int W_PRODA = 4 * NDS + 6;            // activation + s/z producer
-  static constexpr int W_PRODW = 4 * NDS + 7;            // weight producer (highest priority)
+  // warp roles.  The producers and the TMEM allocator come first: an SM starts a CTA's warps
+  // one after another (measured: the last of 20 warps reached the barrier initialisation ~1800
+  // cycles after warp 0 started), so the setup and the first weight requests go to warp 0.
+  // (Issue priority does not follow warp ids -- reordering roles by id was measured neutral.)
+  static constexpr int W_PRODW = 0;                      // weight producer + barrier init
+  static constexpr int W_PRODA = 1;                      // activation + s/z producer
+  static constexpr int W_MMA = 2;                        // 2 MMA issuer warps (also TMEM allocator)
+  static constexpr int W_SCALE = 4;                      // 4 scale / epilogue warps
+  static constexpr int W_DEQ = 8;                        // 4 * NDS dequant warps
   static constexpr int SZG = 8;
   static constexpr int SZ_BOX = SZG * 128 * 2;
   static constexpr int SZ_SLOTS = 4;                     // s/z boxes in flight (16 chunks of look-ahead)
   static constexpr int TMEM_COLS = 512;
+  // cluster split: the leader receives CS - 1 fp32 partials (NT x 128) in its weight ring
+  static constexpr int MAX_CLUSTER = 1 + (NW * W_BYTES) / (NT * 512) < 8 ? 1 + (NW * W_BYTES) / (NT * 512) : 8;
   static constexpr int HDR = 1024;
   static constexpr int SMEM = 1024 + HDR + NW * W_BYTES + NA * ACT_BYTES + SZ_SLOTS * 2 * SZ_BOX;
   static_assert(DAVAIL >= 4 * NT, "TMEM: one chunk of g = 64 D slots");
@@ -115,11 +119,13 @@ __device__ __forceinline__ int dec_nissue(int dring) {
   return (dring >= 2 && DecCfg<NT>::NA % 2 == 0) ? 2 : 1;
 }
 
-__device__ __forceinline__ int dec_owner(long long u, long long T, int P) {
+// 32-bit unsigned arithmetic (the host guarantees T * P < 2^32): a 64-bit division is a
+// ~100-instruction subroutine and sat on every warp's prologue
+__device__ __forceinline__ int dec_owner(uint32_t u, uint32_t T, uint32_t P) {
   return static_cast<int>(((u + 1) * P - 1) / T);
 }
-__device__ __forceinline__ long long dec_start(int p, long long T, int P) {
-  return (static_cast<long long>(p) * T) / P;
+__device__ __forceinline__ uint32_t dec_start(uint32_t p, uint32_t T, uint32_t P) {
+  return (p * T) / P;
 }
 
 // operand for the integer-exact MMA: x - (MAGIC + z) for the 4 pairs of one LAYOUT v1 word
@@ -207,9 +213,9 @@ struct RingPos {
 
 // Iterate the CTA's segments: a segment is the part of one (m-tile, n-tile) inside [u0, u1).
 #define DEC_FOR_SEGMENTS                                                                            \
-  for (long long u = u0, cend = 0; u < u1; u = cend)                                                \
+  for (uint32_t u = u0, cend = 0; u < u1; u = cend)                                                  \
     if (const int t = static_cast<int>(u / kc); true)                                              \
-      if ((cend = ((static_cast<long long>(t) + 1) * kc < u1 ? (static_cast<long long>(t) + 1) * kc : u1)), true)
+      if ((cend = ((static_cast<uint32_t>(t) + 1) * kc < u1 ? (static_cast<uint32_t>(t) + 1) * kc : u1)), true)
 
 template <int NT, bool BF16, int OUT>
 __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
@@ -254,9 +260,18 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
 
   const int P = gridDim.x;
   const int p = blockIdx.x;
-  const long long T = args.total;
-  const long long u0 = dec_start(p, T, P);
-  const long long u1 = dec_start(p + 1, T, P);
+  const uint32_t T = static_cast<uint32_t>(args.total);
+  const int CS = args.cluster;
+  uint32_t u0, u1;
+  if (CS > 0) {  // CS CTAs per tile: rank r takes chunks [r kc / CS, (r + 1) kc / CS) of tile p / CS
+    const uint32_t tl = static_cast<uint32_t>(p / CS) * args.kc, r = static_cast<uint32_t>(p % CS);
+    u0 = tl + (r * args.kc) / CS;
+    u1 = tl + ((r + 1) * args.kc) / CS;
+  } else {
+    u0 = dec_start(p, T, P);
+    u1 = dec_start(p + 1, T, P);
+  }
+  float acc_keep[NT];  // scale warps, cluster split: this CTA's partial until the cluster reduction
   const int KS = args.K / 64;
   const int kc = args.kc;
   const int gshift = args.group == 64 ? 6 : 7;
@@ -278,8 +293,8 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
     int i = 0;
     DEC_FOR_SEGMENTS {
       const int nt = t % args.n_tiles;
-      const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
-      const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
+      const int c0 = static_cast<int>(u - static_cast<uint32_t>(t) * kc);
+      const int c1 = static_cast<int>(cend - static_cast<uint32_t>(t) * kc);
       for (int c = c0; c < c1; ++c, ++i) {
         if (i < w_i) continue;
         if (i >= i_end) return;
@@ -308,6 +323,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
     }
   };
   if (warp == Cfg::W_PRODW) {
+    if (lane == 0) DMARK(10);
     constexpr int NBAR = 2 * NW + 3 * NR + DR_MAX + 2 * Cfg::SZ_SLOTS;
     for (int b = static_cast<int>(lane); b < NBAR; b += 32) {
       uint32_t cnt;
@@ -323,6 +339,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
     }
     fence_mbar_init();
     __syncwarp();
+    if (lane == 0) DMARK(7);
     if (lane == 0) {
       prefetch_tmap(&tmap_a);
       prefetch_tmap(&tmap_s);
@@ -332,8 +349,10 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
     // and the first chunk still landed ~5900 cycles after the CTA start -- HBM latency)
   }
   if (warp == Cfg::W_MMA) {
+    if (lane == 0) DMARK(9);
     tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
     tmem_relinquish();
+    if (lane == 0) DMARK(8);
   }
   tc_fence_before();
   __syncthreads();
@@ -375,7 +394,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         DACC(138, 0);
       }
     }
-  } else if ((TM_DIAG & 32768) && (warp == Cfg::W_PRODW || warp < Cfg::W_SCALE)) {
+  } else if ((TM_DIAG & 32768) && (warp == Cfg::W_PRODW || warp >= Cfg::W_DEQ)) {
     // diagnostic: no weight producer, no dequant
   } else if ((TM_DIAG & 16384) && warp >= Cfg::W_SCALE && warp < Cfg::W_SCALE + 4) {
     // diagnostic: no scale warps
@@ -390,8 +409,8 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
     DEC_FOR_SEGMENTS {
       const int mt = t / args.n_tiles;
       const int nt = t % args.n_tiles;
-      const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
-      const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
+      const int c0 = static_cast<int>(u - static_cast<uint32_t>(t) * kc);
+      const int c1 = static_cast<int>(cend - static_cast<uint32_t>(t) * kc);
       for (int c = c0; c < c1; ++c, ++i) {
         if (((c - c0) & box_mask) == 0) {  // s/z do not depend on the previous kernel
           const int j = box % Cfg::SZ_SLOTS;
@@ -444,8 +463,8 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
       int i = 0, ac = 0;
       RingPos rp;
       DEC_FOR_SEGMENTS {
-        const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
-        const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
+        const int c0 = static_cast<int>(u - static_cast<uint32_t>(t) * kc);
+        const int c1 = static_cast<int>(cend - static_cast<uint32_t>(t) * kc);
         for (int c = c0; c < c1; ++c, ++i, rp.advance(NR), ac = (ac + 1 == NDS) ? 0 : ac + 1) {
           if ((i & is_mask) != me) continue;
           const int r = rp.slot;
@@ -518,9 +537,9 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         }
       }
     }
-  } else if (warp < Cfg::W_SCALE) {
+  } else if (warp >= Cfg::W_DEQ) {
     // ---------------------------------------------------------------- dequant (NDS sets)
-    const int set = warp >> 2;  // takes chunks i % NDS == set, TMEM operand slot `set`
+    const int set = (warp - Cfg::W_DEQ) >> 2;  // takes chunks i % NDS == set, TMEM operand slot `set`
     const int quarter = warp & 3;
     const int row = quarter * 32 + static_cast<int>(lane);
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
@@ -529,8 +548,8 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
     RingPos wp, rp, rp_prev;  // weight ring, ready/done ring, and the set's previous chunk's entry
     bool box_ready = false;
     DEC_FOR_SEGMENTS {
-      const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
-      const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
+      const int c0 = static_cast<int>(u - static_cast<uint32_t>(t) * kc);
+      const int c1 = static_cast<int>(cend - static_cast<uint32_t>(t) * kc);
       int g_base = 0;
       for (int c = c0; c < c1; ++c, wp.advance(NW), rp.advance(NR), sel = (sel + 1 == NDS) ? 0 : sel + 1) {
         if (((c - c0) & box_mask) == 0) {
@@ -552,7 +571,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         const long long q0 = DCLK();
         mbar_wait(bar_fullw + 8 * ws, wp.phase);  // the chunk's packed weights landed
         const long long q1 = DCLK();
-        if (mine == 0 && warp == 0 && lane == 0) DMARK(2);
+        if (mine == 0 && warp == Cfg::W_DEQ && lane == 0) DMARK(2);
         const uint8_t* wst = w_ptr0 + ws * Cfg::W_BYTES + row * 16;
         // zero operands of the chunk's groups (g = 128: 2, g = 64: 4), before the slot wait
         const int gi0 = ((kb0 * 64) >> gshift) - g_base;
@@ -607,9 +626,9 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         const long long q4 = DCLK();
         if (!(TM_DIAG & 8192)) tc_fence_before();
         mbar_arrive(bar_ready + 8 * r);
-        if (lane == 0 && (warp & 3) == 0) DMARK(3);  // last chunk's operands written (latest wins)
+        if (lane == 0 && quarter == 0) DMARK(3);  // last chunk's operands written (latest wins)
         ++mine;
-        if (warp == 0 && lane == 0) {
+        if (warp == Cfg::W_DEQ && lane == 0) {
           DACC(143, q1 - q0);
           DACC(144, q2 - q1);
           DACC(146, DCLK() - q2);
@@ -631,8 +650,8 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
     DEC_FOR_SEGMENTS {
       const int nt = t % args.n_tiles;
       const int mt = t / args.n_tiles;
-      const int c0 = static_cast<int>(u - static_cast<long long>(t) * kc);
-      const int c1 = static_cast<int>(cend - static_cast<long long>(t) * kc);
+      const int c0 = static_cast<int>(u - static_cast<uint32_t>(t) * kc);
+      const int c1 = static_cast<int>(cend - static_cast<uint32_t>(t) * kc);
       float acc[NT];
 #pragma unroll
       for (int m = 0; m < NT; ++m) acc[m] = 0.f;
@@ -709,12 +728,16 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
       // contributors' flags (long set by then), adds their partials in fixed CTA order
       // (deterministic) and stores.  A tail only stores its partial and raises its flag.
       const long long qe = DCLK();
-      const long long tile_lo = static_cast<long long>(t) * kc;
-      const long long tile_hi = tile_lo + kc;
+      const uint32_t tile_lo = static_cast<uint32_t>(t) * kc;
+      const uint32_t tile_hi = tile_lo + kc;
       const int n = nt * 128 + row;
       const int mb = mt * NT;
       const int mcount = (args.M - mb) < NT ? (args.M - mb) : NT;
-      if (u != tile_lo) {
+      if (CS > 1) {
+        // cluster split: reduced through distributed shared memory after the CTA-wide sync
+#pragma unroll
+        for (int m = 0; m < NT; ++m) acc_keep[m] = acc[m];
+      } else if (u != tile_lo) {
         // tail / middle piece: always this CTA's first segment -> partial slot p, flag p
         float* ws = args.workspace + static_cast<size_t>(p) * NT * 128;
 #pragma unroll
@@ -764,6 +787,37 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
   if (warp == Cfg::W_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+  if (CS > 1) {
+    // ---- cluster split-K reduction (DSMEM): ranks 1..CS-1 write their fp32 partials into the
+    // leader's (now idle) weight ring, the leader adds them in rank order (deterministic) and
+    // stores.  Barrier 1: every CTA is done with its rings; barrier 2: partials landed.
+    const uint32_t rank = cluster_ctarank();
+    const bool scale = warp >= Cfg::W_SCALE && warp < Cfg::W_SCALE + 4;
+    const int row = (warp & 3) * 32 + static_cast<int>(lane);
+    cluster_arrive();
+    cluster_wait();
+    if (scale && rank > 0) {
+      const uint32_t dst = mapa_shared(w0 + ((rank - 1) * NT * 128 + row) * 4, 0);
+#pragma unroll
+      for (int m = 0; m < NT; ++m) st_cluster_f32(dst + m * 128 * 4, acc_keep[m]);
+    }
+    cluster_arrive();
+    cluster_wait();
+    if (scale && rank == 0) {
+      const float* red = reinterpret_cast<const float*>(w_ptr0);
+      for (int q = 1; q < CS; ++q) {
+#pragma unroll
+        for (int m = 0; m < NT; ++m) acc_keep[m] += red[(q - 1) * NT * 128 + m * 128 + row];
+      }
+      const int t = p / CS;
+      const int n = (t % args.n_tiles) * 128 + row;
+      const int mb = (t / args.n_tiles) * NT;
+      const int mcount = (args.M - mb) < NT ? (args.M - mb) : NT;
+#pragma unroll
+      for (int m = 0; m < NT; ++m)
+        if (m < mcount) dec_store<BF16, OUT>(args.out, args.N, mb + m, n, acc_keep[m]);
+    }
   }
 }
 

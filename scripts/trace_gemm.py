@@ -95,10 +95,19 @@ if t[:, 140].max() > 0:  # built with TM_PROFILE=1
     if t[:, 2].max() > 0:
         g0 = t[:, 0]
         print("timeline (cycles since CTA start, p50/p90/max over CTAs):")
-        for k, name in {1: "setup done", 2: "first weights landed", 3: "last operands written", 4: "last accumulation done",
+        for k, name in {10: "prologue computed", 9: "MMA warp starts", 8: "TMEM allocated", 7: "barriers initialised", 1: "setup done", 2: "first weights landed", 3: "last operands written", 4: "last accumulation done",
                         5: "epilogue done"}.items():
             x = t[:, k]
             print(f"   {name:24s} {np.percentile(x,50):8.0f} {np.percentile(x,90):8.0f} {x.max():8.0f}")
         start_ns = (g0 - g0.min())
         end_ns = (t[:, 6] - g0.min())
         print(f"   CTA start spread ns: p50 {np.percentile(start_ns,50):.0f} max {start_ns.max():.0f}; CTA end (ns from first start): p50 {np.percentile(end_ns,50):.0f} max {end_ns.max():.0f}")
+    if t[:, 6].max() > 0:
+        g0 = t[:, 0].astype(np.int64)
+        start_ns = g0 - g0.min()
+        end_ns = t[:, 6].astype(np.int64) - g0.min()
+        order = np.argsort(-end_ns)[:8]
+        print("slowest CTAs: idx start_ns end_ns | first_w last_op last_acc epi_done (cycles)")
+        for c in order:
+            print(f"   {c:4d} {start_ns[c]:7d} {end_ns[c]:7d} | {t[c,2]:6d} {t[c,3]:6d} {t[c,4]:6d} {t[c,5]:6d}")
+        print("CTA start ns by index (every 16th):", start_ns[::16].tolist())

@@ -251,3 +251,45 @@ def test_streamk_deterministic_and_counter_reset():
     outs = [bits16(api.gemm_w4a16(t["A"], p, t["s"], t["z"])) for _ in range(4)]
     assert all(np.array_equal(outs[0], o) for o in outs[1:])
     _assert_parity(api.gemm_w4a16(t["A"], p, t["s"], t["z"]), d)
+
+
+CLUSTER_CASES = [2, 3, 4, 5, 8]
+
+
+@pytest.mark.parametrize("cs", CLUSTER_CASES)
+@pytest.mark.parametrize("group", [64, 128])
+def test_decode_cluster_split_ragged(cs, group):
+    """Decode kernel in cluster mode (cs CTAs per tile, DSMEM reduction in rank order):
+    ragged M (all three tile sizes), K tails, cs capped by K and by the leader's SMEM."""
+    api.set_gemm_override(0, 0)
+    api.set_decode_cluster(cs)
+    try:
+        for M, N, K in ((1, 384, 896), (16, 256, 2048), (19, 512, 640), (33, 384, 1408), (64, 256, 4096)):
+            d = synth.awq_like(M, N, K, group=group, seed=M * 11 + N + K + cs)
+            cfg = api.query_gemm_config(M, N, K)
+            assert cfg["kind"] == 2 and 2 <= cfg["split_k"] <= cs, cfg
+            C, _, _ = _run(d)
+            _assert_parity(C, d, tag=(cs, M, N, K))
+    finally:
+        api.set_decode_cluster(0)
+
+
+def test_decode_cluster_auto_shapes_and_determinism():
+    """Automatic choice on Llama-3-8B o_proj / qkv (cluster mode) is bit-stable run to run and
+    within tolerance; partial f32 and fp16 variants."""
+    api.set_gemm_override(0, 0)
+    api.set_decode_cluster(0)
+    for (M, N, K) in ((16, 4096, 4096), (8, 6144, 4096)):
+        assert api.query_gemm_config(M, N, K)["kind"] == 2
+        d = synth.awq_like(M, N, K, seed=N + M)
+        t = to_dev(d)
+        p = api.pack_w4(t["q"], t["s"], t["z"], 128)
+        outs = [bits16(api.gemm_w4a16(t["A"], p, t["s"], t["z"])) for _ in range(3)]
+        assert all(np.array_equal(outs[0], o) for o in outs[1:])
+        _assert_parity(api.gemm_w4a16(t["A"], p, t["s"], t["z"]), d)
+    d = synth.awq_like(9, 1024, 1024, seed=79)
+    C, _, _ = _run(d, out="f32")
+    _assert_parity(C, d, act="fp32")
+    d16 = synth.awq_like(9, 1024, 1024, seed=80, act_dtype="fp16")
+    C16, _, _ = _run(d16, act="fp16")
+    _assert_parity(C16, d16, act="fp16")

@@ -53,15 +53,24 @@ def test_host_only_entry_points():
 
 def test_config_selection_host_logic():
     api.set_gemm_override(0, 0)
-    c = api.query_gemm_config(16, 4096, 4096)  # decode: persistent stream-K, one CTA per SM
-    assert c["tile_m"] == 16 and c["split_k"] < 0 and c["grid_ctas"] == -c["split_k"]
-    assert c["grid_ctas"] <= 32 * 16  # never more CTAs than 256-k chunks
+    c = api.query_gemm_config(16, 28672, 4096)  # decode, many tiles: persistent stream-K
+    assert c["tile_m"] == 16 and c["split_k"] < 0 and c["grid_ctas"] == -c["split_k"] and c["kind"] == 1
+    assert c["grid_ctas"] <= 224 * 16  # never more CTAs than 256-k chunks
+    c = api.query_gemm_config(16, 4096, 4096)  # decode, 32 tiles x 16 chunks: 2 CTAs per tile
+    assert c == dict(tile_m=16, split_k=2, grid_ctas=64, kind=2)
+    c = api.query_gemm_config(16, 4096, 14336)  # 32 tiles x 56 chunks: 4 CTAs per tile
+    assert c == dict(tile_m=16, split_k=4, grid_ctas=128, kind=2)
+    api.set_decode_cluster(1)  # never: stream-K
+    assert api.query_gemm_config(16, 4096, 4096)["kind"] == 1
+    api.set_decode_cluster(3)
+    assert api.query_gemm_config(16, 4096, 4096) == dict(tile_m=16, split_k=3, grid_ctas=96, kind=2)
+    api.set_decode_cluster(0)
     c = api.query_gemm_config(1, 128, 256)
     assert c["grid_ctas"] == 1  # one tile of one chunk
     c = api.query_gemm_config(4096, 4096, 4096)
     assert c["tile_m"] == 256 and c["split_k"] == 1 and c["grid_ctas"] == 32 * 16
     api.set_gemm_override(64, 3)
-    assert api.query_gemm_config(5, 256, 1024) == dict(tile_m=64, split_k=3, grid_ctas=6)
+    assert api.query_gemm_config(5, 256, 1024) == dict(tile_m=64, split_k=3, grid_ctas=6, kind=0)
     api.set_gemm_override(0, 0)
     try:
         api.set_gemm_override(48, 0)
