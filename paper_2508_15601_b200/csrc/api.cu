@@ -110,6 +110,39 @@ tm_status act_tensor_map(const void* A, int M, int K, int NT, bool bf16, CUtenso
   return TM_OK;
 }
 
+// 2-D output map for the tiled kernel's TMA-store epilogue: dims {N, M}, box {128, rows}
+tm_status out_tensor_map(void* C, int M, int N, int NT, int esize, bool bf16, CUtensorMap* out) {
+  const MapKey key{C, M, N, 1000 + NT * 8 + esize, bf16 ? 1 : 0};
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return TM_OK;
+    }
+  }
+  auto enc = get_encode();
+  if (!enc) return TM_ERR_CUDA;
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(N) * esize};
+  const int rows = esize == 4 && NT > 128 ? 128 : (NT < 256 ? NT : 256);
+  const cuuint32_t box[2] = {128, static_cast<cuuint32_t>(rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapDataType dt = esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                           : (bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+  CUresult r = enc(&map, dt, 2, C, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return TM_ERR_CUDA;
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    if (g_maps.size() > 4096) g_maps.clear();
+    g_maps.emplace(key, map);
+  }
+  *out = map;
+  return TM_OK;
+}
+
 // 3-D activation map for the stream-K kernel: dims {64, M, K/64}, strides {2K, 128} bytes,
 // box {64, NT, CH/64}: one request lands CH/64 SW128 sub-tiles of NT x 64.
 tm_status act_tensor_map_3d(const void* A, int M, int K, int NT, int blobs, bool bf16, CUtensorMap* out) {
@@ -405,7 +438,10 @@ tm_status launch_gemm_t(const CUtensorMap& map, const GemmArgs& args, const Conf
   ++na;
   cfg.attrs = attrs;
   cfg.numAttrs = na;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, args);
+  CUtensorMap cmap;
+  const tm_status cst = out_tensor_map(args.out, args.M, args.N, NT, OUT == OUT_F32 ? 4 : 2, BF16, &cmap);
+  if (cst != TM_OK) return cst;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, cmap, args);
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
     return TM_ERR_CUDA;
