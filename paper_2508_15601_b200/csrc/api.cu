@@ -438,10 +438,14 @@ tm_status launch_gemm_t(const CUtensorMap& map, const GemmArgs& args, const Conf
   ++na;
   cfg.attrs = attrs;
   cfg.numAttrs = na;
-  CUtensorMap cmap;
-  const tm_status cst = out_tensor_map(args.out, args.M, args.N, NT, OUT == OUT_F32 ? 4 : 2, BF16, &cmap);
+  CUtensorMap cmap, smap, zmap;
+  tm_status cst = out_tensor_map(args.out, args.M, args.N, NT, OUT == OUT_F32 ? 4 : 2, BF16, &cmap);
   if (cst != TM_OK) return cst;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, cmap, args);
+  cst = sz_tensor_map(args.scales, args.K / args.group, args.N, &smap);
+  if (cst != TM_OK) return cst;
+  cst = sz_tensor_map(args.zeros, args.K / args.group, args.N, &zmap);
+  if (cst != TM_OK) return cst;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, cmap, smap, zmap, args);
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
     return TM_ERR_CUDA;

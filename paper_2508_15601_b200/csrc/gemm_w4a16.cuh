@@ -33,8 +33,9 @@ namespace w4k {
 constexpr int kBN = 128;          // weight columns per CTA tile (= TMEM lanes)
 constexpr int kBK = 64;           // k per pipeline stage
 constexpr int kBlobBytes = 4096;  // packed bytes per (n-tile, k-stage)
-constexpr int kSZBytes = 512;     // s row (256 B) + z row (256 B) per stage
-constexpr int kThreads = 192;     // 6 warps
+constexpr int kSZBox = 8 * kBN * 2;  // one TMA box: 8 groups x 128 columns of fp16 (s or z)
+constexpr int kSZSlots = 2;          // s/z box ring
+constexpr int kThreads = 256;        // 8 warps (registers are allocated per SM sub-partition)
 
 enum OutKind { OUT_ACT = 0, OUT_F32 = 1 };
 
@@ -68,7 +69,7 @@ struct GemmCfg {
   static constexpr int TMEM_NEED = ACC_COLS + ASTAGES * 32;
   static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
   static constexpr int HDR = 1024;  // barriers + tmem pointer
-  static constexpr int RING = STAGES * (ACT_BYTES + kBlobBytes + kSZBytes);
+  static constexpr int RING = STAGES * (ACT_BYTES + kBlobBytes) + kSZSlots * 2 * kSZBox;
   // largest split-K whose DSMEM reduction buffer fits next to the header (<= ~200 KB)
   static constexpr int MAX_SPLIT = (1 + (200 * 1024) / (NT * kBN * 4)) < 8 ? (1 + (200 * 1024) / (NT * kBN * 4)) : 8;
   static int smem_bytes(int split) {
@@ -84,6 +85,7 @@ struct GemmCfg {
 template <int NT, bool BF16, int OUT>
 __global__ void __launch_bounds__(kThreads, 1)
     w4a16_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_c,
+                      const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CUtensorMap tmap_z,
                       const GemmArgs args) {
   using Cfg = GemmCfg<NT>;
   constexpr int STAGES = Cfg::STAGES;
@@ -98,13 +100,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t bar_afull = bar_empty + 8 * STAGES;      // ASTAGES x 8 B
   const uint32_t bar_aempty = bar_afull + 8 * ASTAGES;    // ASTAGES x 8 B
   const uint32_t bar_acc = bar_aempty + 8 * ASTAGES;      // 8 B
-  const uint32_t tmem_slot = bar_acc + 8;                 // 4 B
+  const uint32_t bar_szfull = bar_acc + 8;                // kSZSlots x 8 B (producer W, tx)
+  const uint32_t bar_szempty = bar_szfull + 8 * kSZSlots; // kSZSlots x 8 B (128 dequant threads)
+  const uint32_t tmem_slot = bar_szempty + 8 * kSZSlots;  // 4 B
   uint32_t* const tmem_slot_ptr = reinterpret_cast<uint32_t*>(base_ptr + (tmem_slot - base));
   // ring
   const uint32_t ring = base + Cfg::HDR;
   const uint32_t act0 = ring;                                    // STAGES x ACT_BYTES
   const uint32_t blob0 = act0 + STAGES * Cfg::ACT_BYTES;         // STAGES x 4096
-  const uint32_t sz0 = blob0 + STAGES * kBlobBytes;              // STAGES x 512
+  const uint32_t sz0 = blob0 + STAGES * kBlobBytes;              // kSZSlots x [s box | z box]
   uint8_t* const ring_ptr = base_ptr + Cfg::HDR;
   const uint8_t* const blob_ptr0 = ring_ptr + STAGES * Cfg::ACT_BYTES;
   const uint8_t* const sz_ptr0 = blob_ptr0 + STAGES * kBlobBytes;
@@ -129,9 +133,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmap_a);
+    prefetch_tmap(&tmap_s);
+    prefetch_tmap(&tmap_z);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_full + 8 * s, 2);         // weight producer + activation producer
       mbar_init(bar_empty + 8 * s, 128 + 1);  // 128 dequant threads + 1 MMA commit
+    }
+    for (int j = 0; j < kSZSlots; ++j) {
+      mbar_init(bar_szfull + 8 * j, 1);
+      mbar_init(bar_szempty + 8 * j, 128);
     }
     for (int a = 0; a < ASTAGES; ++a) {
       mbar_init(bar_afull + 8 * a, 128);
@@ -155,34 +165,59 @@ __global__ void __launch_bounds__(kThreads, 1)
   // PDL: everything above overlaps the previous kernel's tail; global reads start below.
   grid_dependency_wait();
 
+  // groups of this CTA's K range; s/z arrive as 8-group x 128-column TMA boxes
+  const int gshift = args.group == 64 ? 6 : 7;
+  const int g_start = (ks0 * kBK) >> gshift;
   if (warp == 0) {
-    // ------------------------------------------------------------ producer
+    // ------------------------------------------------------------ producer W: weights + s/z
+    // (one request per stage here and one per stage on the activation producer: a bulk/TMA
+    // request costs its issuing warp ~300 cycles, four per stage on one warp paced the loop)
     if (lane == 0) {
       const uint8_t* blob_g = args.packed + (static_cast<size_t>(nt) * KS + ks0) * kBlobBytes;
       const uint64_t pol_stream = policy_evict_first();
       const bool stream_weights = gridDim.y == 1;  // weights read once: do not keep them in L2
       TM_TRACE(2);
+      int box = -1;
       for (int i = 0; i < nks; ++i) {
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
+        const int gb = ((((ks0 + i) * kBK) >> gshift) - g_start) >> 3;  // box of this stage
+        if (gb != box) {
+          box = gb;
+          const int j = box % kSZSlots;
+          mbar_wait(bar_szempty + 8 * j, ((box / kSZSlots) & 1) ^ 1);
+          const uint32_t fb = bar_szfull + 8 * j;
+          mbar_arrive_expect_tx(fb, 2 * kSZBox);
+          tma_load_2d(sz0 + j * 2 * kSZBox, &tmap_s, nt * kBN, g_start + 8 * box, fb);
+          tma_load_2d(sz0 + j * 2 * kSZBox + kSZBox, &tmap_z, nt * kBN, g_start + 8 * box, fb);
+        }
         mbar_wait(bar_empty + 8 * s, ph ^ 1);
         if (i < 32) TM_TRACE(3 + i);
-        const int ks = ks0 + i;
-        const int g = (ks * kBK) / args.group;
         const uint32_t fb = bar_full + 8 * s;
-        mbar_arrive_expect_tx(fb, kBlobBytes + kSZBytes + Cfg::ACT_BYTES);
+        mbar_arrive_expect_tx(fb, kBlobBytes);
         if (stream_weights)
           bulk_g2s_hint(blob0 + s * kBlobBytes, blob_g + static_cast<size_t>(i) * kBlobBytes, kBlobBytes, fb,
                         pol_stream);
         else
           bulk_g2s(blob0 + s * kBlobBytes, blob_g + static_cast<size_t>(i) * kBlobBytes, kBlobBytes, fb);
-        const size_t szoff = static_cast<size_t>(g) * args.N + static_cast<size_t>(nt) * kBN;
-        bulk_g2s(sz0 + s * kSZBytes, args.scales + szoff, 256, fb);
-        bulk_g2s(sz0 + s * kSZBytes + 256, args.zeros + szoff, 256, fb);
-        tma_load_2d(act0 + s * Cfg::ACT_BYTES, &tmap_a, ks * kBK, m0, fb);
       }
     }
     __syncwarp();
+  } else if (warp == 6) {
+    // ------------------------------------------------------------ producer A: activations
+    if (lane == 0) {
+      for (int i = 0; i < nks; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(bar_empty + 8 * s, ph ^ 1);
+        const uint32_t fb = bar_full + 8 * s;
+        mbar_arrive_expect_tx(fb, Cfg::ACT_BYTES);
+        tma_load_2d(act0 + s * Cfg::ACT_BYTES, &tmap_a, (ks0 + i) * kBK, m0, fb);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 7) {
+    // spare warp (keeps the CTA a multiple of 4 warps)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
@@ -213,18 +248,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int row = quarter * 32 + static_cast<int>(lane);
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    int box = -1;
     for (int i = 0; i < nks; ++i) {
       const int s = i % STAGES;
       const uint32_t ph = (i / STAGES) & 1;
       const int a = i % ASTAGES;
       const uint32_t aph = (i / ASTAGES) & 1;
+      const int gl = (((ks0 + i) * kBK) >> gshift) - g_start;  // group within this CTA's range
+      if ((gl >> 3) != box) {
+        if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % kSZSlots));
+        box = gl >> 3;
+        mbar_wait(bar_szfull + 8 * (box % kSZSlots), (box / kSZSlots) & 1);
+      }
       mbar_wait(bar_full + 8 * s, ph);
       if (i < 32 && warp == 2 && lane == 0) TM_TRACE(35 + i);
       const uint8_t* blob = blob_ptr0 + s * kBlobBytes;
       const uint4 w0 = *reinterpret_cast<const uint4*>(blob + row * 16);
       const uint4 w1 = *reinterpret_cast<const uint4*>(blob + 2048 + row * 16);
-      const uint16_t sb = *reinterpret_cast<const uint16_t*>(sz_ptr0 + s * kSZBytes + row * 2);
-      const uint16_t zb = *reinterpret_cast<const uint16_t*>(sz_ptr0 + s * kSZBytes + 256 + row * 2);
+      const uint8_t* szb = sz_ptr0 + (box % kSZSlots) * 2 * kSZBox + ((gl & 7) * kBN + row) * 2;
+      const uint16_t sb = *reinterpret_cast<const uint16_t*>(szb);
+      const uint16_t zb = *reinterpret_cast<const uint16_t*>(szb + kSZBox);
       mbar_arrive(bar_empty + 8 * s);
       uint32_t s2, z2;
       deq_prepare<BF16>(sb, zb, s2, z2);
@@ -245,6 +288,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(bar_afull + 8 * a);
       if (i < 32 && warp == 2 && lane == 0) TM_TRACE(67 + i);
     }
+
+    if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % kSZSlots));
 
     // ------------------------------------------------------------ epilogue
     mbar_wait(bar_acc, 0);
@@ -340,8 +385,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
-  if (S > 1 && warp < 2) {
-    // producer and MMA warps take part in the two cluster barriers of the epilogue
+  if (S > 1 && (warp < 2 || warp >= 6)) {
+    // producer, MMA and spare warps take part in the two cluster barriers of the epilogue
     cluster_arrive();
     cluster_wait();
     cluster_arrive();
