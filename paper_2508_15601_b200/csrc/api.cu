@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -332,7 +333,9 @@ Config choose_config(int M, int N, int K) {
     nt = 32;
   } else if (M <= 64) {
     nt = 64;
-  } else if (M <= 128) {
+  } else if (M <= 128 || (M <= 256 && 2 * (N / 128) <= num_sms())) {
+    // (mid M: 128-token tiles while 2 m-tiles of them still fit one wave -- measured o_proj
+    // M=256 23.7 us at NT=128 + split 2 vs 29.0 us at NT=256)
     nt = 128;
   } else {
     nt = 256;
@@ -394,6 +397,19 @@ Config choose_config(int M, int N, int K) {
     const int target = 2 * num_sms();
     split = (target + tiles - 1) / tiles;
     if (split > 8) split = 8;
+  } else {
+    // mid M: few tiles leave SMs idle while every CTA dequantises its whole K range, so split K
+    // over a cluster of up to 4 while the clusters still pack into one wave (<= 128 CTAs; a
+    // 144-CTA layout of 3-clusters spilled into a second wave).  Graph-timed (scripts/mid_sweep3.py):
+    // o M=128 28.4 -> 20.5 us (s4), down M=128 89.5 -> 36.1 (s4), qkv M=128 28.3 -> 23.0 (s2),
+    // down M=512 89.3 -> 62.5 (s2)
+    const int tiles = n_tiles * m_tiles;
+    split = 1;
+    for (int k = 4; k >= 2; --k)
+      if (tiles * k <= 128) {
+        split = k;
+        break;
+      }
   }
   if (split > KS) split = KS;
   if (split > max_split_for(nt)) split = max_split_for(nt);
@@ -506,10 +522,10 @@ tm_status launch_sk_t(const void* A, const GemmArgs& g, const Config& c, cudaStr
   return TM_OK;
 }
 
-template <int NT, bool BF16, int OUT>
+template <int NT, bool BF16, int OUT, bool FS>
 tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream) {
-  using Cfg = DecCfg<NT>;
-  auto kern = w4a16_dec_kernel<NT, BF16, OUT>;
+  using Cfg = DecCfg<NT, FS>;
+  auto kern = w4a16_dec_kernel<NT, BF16, OUT, FS>;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess) {
@@ -549,16 +565,20 @@ tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaSt
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attrs[2];
-  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attrs[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 0;
+  static const bool no_pdl = std::getenv("TM_NO_PDL") != nullptr;  // experiments only
+  if (!no_pdl) {
+    attrs[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+    ++cfg.numAttrs;
+  }
   if (c.kind == 2 && c.split > 1) {
-    attrs[1].id = cudaLaunchAttributeClusterDimension;
-    attrs[1].val.clusterDim.x = c.split;
-    attrs[1].val.clusterDim.y = 1;
-    attrs[1].val.clusterDim.z = 1;
-    cfg.numAttrs = 2;
+    attrs[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
+    attrs[cfg.numAttrs].val.clusterDim.x = c.split;
+    attrs[cfg.numAttrs].val.clusterDim.y = 1;
+    attrs[cfg.numAttrs].val.clusterDim.z = 1;
+    ++cfg.numAttrs;
   }
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, ms, mz, a);
   if (e != cudaSuccess) {
@@ -571,9 +591,16 @@ tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaSt
 template <bool BF16, int OUT>
 tm_status launch_sk(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream) {
   switch (c.NT) {
-    case 16: return launch_dec_t<16, BF16, OUT>(A, g, c, stream);
-    case 32: return launch_dec_t<32, BF16, OUT>(A, g, c, stream);
-    case 64: return launch_dec_t<64, BF16, OUT>(A, g, c, stream);
+    case 16: {
+      // group 128: dequant sets apply the group scales themselves (no scale warps)
+      static const bool no_fs = std::getenv("TM_NO_FS") != nullptr;  // experiments only
+      // (cluster split-K only: in stream-K mode the sets' segment-end barriers drain the pipeline
+      // mid-range -- measured gate_up M=16 17.4 -> 19.0 us -- while cluster CTAs have one segment)
+      if (g.group == 128 && c.kind == 2 && !no_fs) return launch_dec_t<16, BF16, OUT, true>(A, g, c, stream);
+      return launch_dec_t<16, BF16, OUT, false>(A, g, c, stream);
+    }
+    case 32: return launch_dec_t<32, BF16, OUT, false>(A, g, c, stream);
+    case 64: return launch_dec_t<64, BF16, OUT, false>(A, g, c, stream);
     case 128: return launch_sk_t<128, BF16, OUT>(A, g, c, stream);
     case 256: return launch_sk_t<256, BF16, OUT>(A, g, c, stream);
     default: return TM_ERR_INVALID_ARG;

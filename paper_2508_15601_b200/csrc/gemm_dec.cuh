@@ -48,6 +48,16 @@
 
 namespace w4k {
 
+#ifndef TM_CLUSTER_V2
+#define TM_CLUSTER_V2 0
+#endif
+#ifndef TM_EARLY_W
+#define TM_EARLY_W 0
+#endif
+#ifndef TM_SCALE_TOP
+#define TM_SCALE_TOP 0
+#endif
+
 
 struct DecArgs {
   const uint8_t* packed;  // LAYOUT v1
@@ -63,7 +73,7 @@ struct DecArgs {
   uint32_t* trace;
 };
 
-template <int NT>
+template <int NT, bool FS = false>
 struct DecCfg {
   static constexpr int CH = 256;                         // k per chunk
   static constexpr int BLOBS = 4;                        // LAYOUT v1 blobs per chunk
@@ -75,7 +85,9 @@ struct DecCfg {
   static constexpr int DCOLS = NT;                       // one D_g slot
   static constexpr int DAVAIL = 512 - NDS * BLOBS * 32;  // TMEM columns left for the D ring
   static constexpr int DR_MAX = 4;                       // D ring entries (chunks); runtime: dec_dring()
-  static constexpr int THREADS = 32 * (8 + 4 * NDS);     // a multiple of 4 warps (per-SMSP registers)
+  // FS (fused scale, group 128): no scale warps -- dequant set j also applies the group scales
+  // to the D of its own chunks (its D region: 2 groups x NT columns after the operand slots)
+  static constexpr int THREADS = 32 * ((FS ? 4 : 8) + 4 * NDS);   // a multiple of 4 warps
   // warp roles.  The producers and the TMEM allocator come first: an SM starts a CTA's warps
   // one after another (measured: the last of 20 warps reached the barrier initialisation ~1800
   // cycles after warp 0 started), so the setup and the first weight requests go to warp 0.
@@ -83,8 +95,9 @@ struct DecCfg {
   static constexpr int W_PRODW = 0;                      // weight producer + barrier init
   static constexpr int W_PRODA = 1;                      // activation + s/z producer
   static constexpr int W_MMA = 2;                        // 2 MMA issuer warps (also TMEM allocator)
-  static constexpr int W_SCALE = 4;                      // 4 scale / epilogue warps
-  static constexpr int W_DEQ = 8;                        // 4 * NDS dequant warps
+  // TM_SCALE_TOP: scale warps take the highest ids (the SMSP arbiter favours high warp ids)
+  static constexpr int W_SCALE = FS ? 4 : (TM_SCALE_TOP ? 4 + 4 * NDS : 4);   // 4 scale / epilogue warps
+  static constexpr int W_DEQ = (FS || TM_SCALE_TOP) ? 4 : 8;               // 4 * NDS dequant warps
   static constexpr int SZG = 8;
   static constexpr int SZ_BOX = SZG * 128 * 2;
   static constexpr int SZ_SLOTS = 4;                     // s/z boxes in flight (16 chunks of look-ahead)
@@ -92,8 +105,11 @@ struct DecCfg {
   // cluster split: the leader receives CS - 1 fp32 partials (NT x 128) in its weight ring
   static constexpr int MAX_CLUSTER = 1 + (NW * W_BYTES) / (NT * 512) < 8 ? 1 + (NW * W_BYTES) / (NT * 512) : 8;
   static constexpr int HDR = 1024;
-  static constexpr int SMEM = 1024 + HDR + NW * W_BYTES + NA * ACT_BYTES + SZ_SLOTS * 2 * SZ_BOX;
+  // FS: segment-end deposit of sets 1..NDS-1 (fp32 NT x 128 each)
+  static constexpr int DEP_BYTES = FS ? (NDS - 1) * NT * 128 * 4 : 0;
+  static constexpr int SMEM = 1024 + HDR + NW * W_BYTES + NA * ACT_BYTES + SZ_SLOTS * 2 * SZ_BOX + DEP_BYTES;
   static_assert(DAVAIL >= 4 * NT, "TMEM: one chunk of g = 64 D slots");
+  static_assert(!FS || DAVAIL >= NDS * 2 * NT, "TMEM: FS D regions (group 128)");
   // a ready/done ring entry must be reused by the same dequant set (NA % NDS == 0: that set's
   // previous use is gated by the MMA completion it waits for) -- measured: NA = 4 with 3 sets
   // let a set arrive on an entry whose previous phase the MMA had not yet consumed
@@ -128,14 +144,23 @@ __device__ __forceinline__ uint32_t dec_start(uint32_t p, uint32_t T, uint32_t P
   return (p * T) / P;
 }
 
+#ifndef TM_DEQ_MULHI
+#define TM_DEQ_MULHI 0
+#endif
 // operand for the integer-exact MMA: x - (MAGIC + z) for the 4 pairs of one LAYOUT v1 word
 template <bool BF16>
 __device__ __forceinline__ void deq_word_int(uint32_t w, uint32_t z2, uint32_t* out) {
   constexpr uint32_t MAGIC = BF16 ? 0x43004300u : 0x64006400u;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    // w >> 4i on the ALU pipe (SHF); mul.hi was measured at half rate, so no FMA-pipe shifts
-    const uint32_t ws = w >> (4 * i);
+    // w >> 4i.  The dequant phase is ALU-pipe bound (3 SHF + 4 LOP3 = 14 ALU cycles per word vs
+    // 4 HSUB = 8 FMA cycles), so the last shift runs on the FMA pipe as mul.hi (half rate, 4
+    // cycles): 12 ALU / 12 FMA cycles per word.
+    uint32_t ws;
+    if (TM_DEQ_MULHI && i == 3)
+      asm("mul.hi.u32 %0, %1, %2;" : "=r"(ws) : "r"(w), "r"(1u << 20));
+    else
+      ws = w >> (4 * i);
     uint32_t x;
     asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(x) : "r"(ws), "r"(0x000F000Fu), "r"(MAGIC));
     uint32_t d;
@@ -217,11 +242,11 @@ struct RingPos {
     if (const int t = static_cast<int>(u / kc); true)                                              \
       if ((cend = ((static_cast<uint32_t>(t) + 1) * kc < u1 ? (static_cast<uint32_t>(t) + 1) * kc : u1)), true)
 
-template <int NT, bool BF16, int OUT>
-__global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
+template <int NT, bool BF16, int OUT, bool FS = false>
+__global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
     w4a16_dec_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_s,
                      const __grid_constant__ CUtensorMap tmap_z, const DecArgs args) {
-  using Cfg = DecCfg<NT>;
+  using Cfg = DecCfg<NT, FS>;
   constexpr int NR = Cfg::NA;  // activation slots and per-chunk ready/done barriers
   constexpr int NW = Cfg::NW;
   constexpr int NDS = Cfg::NDS;
@@ -240,11 +265,13 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
   const uint32_t bar_szempty = bar_szfull + 8 * Cfg::SZ_SLOTS;  // SZ_SLOTS (128 NDS dequant + 128 scale)
   const uint32_t tmem_slot = bar_szempty + 8 * Cfg::SZ_SLOTS;
   uint32_t* const tmem_slot_ptr = reinterpret_cast<uint32_t*>(base_ptr + (tmem_slot - base));
+  const uint32_t bar_red = tmem_slot + 16;  // cluster split: partials of ranks 1..CS-1 ready (leader)
   const uint32_t w0 = base + Cfg::HDR;                          // NW x 16 KB packed weights
   const uint32_t a0 = w0 + NW * Cfg::W_BYTES;                   // NR x activation chunk (1 KB aligned)
   const uint32_t sz0 = a0 + NR * Cfg::ACT_BYTES;                // SZ_SLOTS x [s box | z box]
   const uint8_t* const w_ptr0 = base_ptr + Cfg::HDR;
   const uint8_t* const sz_ptr0 = w_ptr0 + NW * Cfg::W_BYTES + NR * Cfg::ACT_BYTES;
+  float* const dep_ptr0 = reinterpret_cast<float*>(const_cast<uint8_t*>(sz_ptr0) + Cfg::SZ_SLOTS * 2 * Cfg::SZ_BOX);
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);  // warp-uniform
   const uint32_t lane = threadIdx.x & 31;
@@ -255,9 +282,22 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
     uint64_t gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
     args.trace[blockIdx.x * 160] = static_cast<uint32_t>(gt);
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    args.trace[blockIdx.x * 160 + 11] = smid;
   }
 #endif
 
+#if TM_PROFILE
+  if (TM_DIAG & 131072) {  // diagnostic: an empty CTA (trace start/end only)
+    if (args.trace && threadIdx.x == 0) {
+      uint64_t gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      args.trace[blockIdx.x * 160 + 6] = static_cast<uint32_t>(gt);
+    }
+    return;
+  }
+#endif
   const int P = gridDim.x;
   const int p = blockIdx.x;
   const uint32_t T = static_cast<uint32_t>(args.total);
@@ -334,9 +374,10 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
       else if (b < 2 * NW + 3 * NR) cnt = 1;                 // done
       else if (b < 2 * NW + 3 * NR + DR_MAX) cnt = 128;      // dfree
       else if (b < NBAR - Cfg::SZ_SLOTS) cnt = 1;            // szfull
-      else cnt = 128 * NDS + 128;                            // szempty
+      else cnt = 128 * NDS + (FS ? 0 : 128);                 // szempty
       mbar_init(bar_fullw + 8 * b, cnt);
     }
+    if (TM_CLUSTER_V2 && CS > 1 && lane == 0) mbar_init(bar_red, (CS - 1) * 128);
     fence_mbar_init();
     __syncwarp();
     if (lane == 0) DMARK(7);
@@ -345,8 +386,9 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
       prefetch_tmap(&tmap_s);
       prefetch_tmap(&tmap_z);
     }
-    // (requesting the first chunks here was measured slower: the setup grew by ~1500 cycles
+    // (requesting all NW first chunks here was measured slower: the setup grew by ~1500 cycles
     // and the first chunk still landed ~5900 cycles after the CTA start -- HBM latency)
+    if (TM_EARLY_W > 0) produce_w(TM_EARLY_W);
   }
   if (warp == Cfg::W_MMA) {
     if (lane == 0) DMARK(9);
@@ -357,6 +399,9 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // cluster split: every thread arrives now and waits at its end, so the leader's bar_red is
+  // initialised before any remote arrive without a cluster-wide stall in the setup
+  if (TM_CLUSTER_V2 && CS > 1) cluster_arrive_relaxed();
   const uint32_t tmem_base = *tmem_slot_ptr;
   if (threadIdx.x == 0) DMARK(1);
   // PDL: let the next kernel in the stream start launching now; its CTAs take SMs as ours exit,
@@ -365,7 +410,60 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
   const uint32_t tmem_a0 = tmem_base;                          // NDS x 4 blobs x 32 columns
   const uint32_t tmem_d0 = tmem_base + NDS * Cfg::BLOBS * 32;  // DR x (256 / g) groups x NT columns
 
-  if (TM_DIAG & 4096) {
+  // ---- segment end (scale warps, or dequant set 0 in FS mode: thread `row` = weight column, et =
+  // its index among the 128 finishing threads).  acc = this CTA's sum over the segment's chunks.
+  const auto seg_end = [&](float (&acc)[NT], int t, uint32_t u, uint32_t cend, int row, int et) {
+    const int nt = t % args.n_tiles;
+    const int mt = t / args.n_tiles;
+    // ---- segment end.  A CTA's range [u0, u1) meets a shared tile only at its two ends: its
+    // first segment may be the tile's tail (or a middle piece), its last segment the tile's
+    // head.  The tail is computed first in time (start of the contributor's range), the head
+    // last (end of the head holder's range), so the head holder finalises: it waits for the
+    // contributors' flags (long set by then), adds their partials in fixed CTA order
+    // (deterministic) and stores.  A tail only stores its partial and raises its flag.
+    const long long qe = DCLK();
+    const uint32_t tile_lo = static_cast<uint32_t>(t) * kc;
+    const uint32_t tile_hi = tile_lo + kc;
+    const int n = nt * 128 + row;
+    const int mb = mt * NT;
+    const int mcount = (args.M - mb) < NT ? (args.M - mb) : NT;
+    if (CS > 1) {
+      // cluster split: reduced through distributed shared memory after the CTA-wide sync
+#pragma unroll
+      for (int m = 0; m < NT; ++m) acc_keep[m] = acc[m];
+    } else if (u != tile_lo) {
+      // tail / middle piece: always this CTA's first segment -> partial slot p, flag p
+      float* ws = args.workspace + static_cast<size_t>(p) * NT * 128;
+#pragma unroll
+      for (int m = 0; m < NT; ++m) __stcg(ws + m * 128 + row, acc[m]);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (et == 0) st_release_gpu(args.counters + p, 1);  // cumulative over the barrier
+    } else {
+      if (cend != tile_hi) {
+        // head of a shared tile (this CTA's last segment): add the later contributors' partials
+        const int p_hi = dec_owner(tile_hi - 1, T, P);
+        if (et == 0)
+          for (int q = p + 1; q <= p_hi; ++q)
+            for (uint32_t spins = 0; ld_acquire_gpu(args.counters + q) == 0;)
+              if (++spins == (1u << 24)) __trap();  // a contributor never arrived: fail, do not hang
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int q = p + 1; q <= p_hi; ++q) {  // fixed k order: deterministic
+          const float* wq = args.workspace + static_cast<size_t>(q) * NT * 128;
+#pragma unroll
+          for (int m = 0; m < NT; ++m) acc[m] += __ldcg(wq + m * 128 + row);
+        }
+        if (et == 0)
+          for (int q = p + 1; q <= p_hi; ++q) args.counters[q] = 0;  // consumed: zero for the next launch
+      }
+#pragma unroll
+      for (int m = 0; m < NT; ++m)
+        if (m < mcount) dec_store<BF16, OUT>(args.out, args.N, mb + m, n, acc[m]);
+    }
+    if (et == 0) DACC(157, DCLK() - qe);
+  };
+  if (TM_DIAG & 65536) {
+    // diagnostic: setup and teardown only
+  } else if (TM_DIAG & 4096) {
     // diagnostic: MMA issuer 0 alone, back-to-back chunks with commit + wait (no other roles)
     if (warp == Cfg::W_MMA) {
       constexpr uint32_t idesc = umma_idesc_f16(BF16, 128, NT);
@@ -480,12 +578,13 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
             if (!(TM_DIAG & 32768)) mbar_wait(bar_ready + 8 * r, rph);  // operands in TMEM
           }
           const long long q1 = DCLK();
-          if (!(TM_DIAG & (1024 | 16384))) mbar_wait(bar_dfree + 8 * dr, ((i >> dr_shift) & 1) ^ 1);  // D slots read
+          // D slots read (FS: the set's D region is free once the set arrived ready for this chunk)
+          if (!FS && !(TM_DIAG & (1024 | 16384))) mbar_wait(bar_dfree + 8 * dr, ((i >> dr_shift) & 1) ^ 1);
           if (!(TM_DIAG & 2048)) tc_fence_after();
           const long long q2 = DCLK();
           long long q3 = q2, qf = q2;
           if (elect_one()) {
-            const uint32_t d_base = tmem_d0 + dr * DSTRIDE;
+            const uint32_t d_base = tmem_d0 + (FS ? ac : dr) * DSTRIDE;
             const uint32_t a_base = tmem_a0 + ac * Cfg::BLOBS * 32;
             // full chunk: 16 MMAs with compile-time operand offsets (no loop-carried address math)
             const auto issue_full = [&](auto bpg_c) {
@@ -537,7 +636,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         }
       }
     }
-  } else if (warp >= Cfg::W_DEQ) {
+  } else if (warp >= Cfg::W_DEQ && warp < Cfg::W_DEQ + 4 * NDS) {
     // ---------------------------------------------------------------- dequant (NDS sets)
     const int set = (warp - Cfg::W_DEQ) >> 2;  // takes chunks i % NDS == set, TMEM operand slot `set`
     const int quarter = warp & 3;
@@ -551,6 +650,9 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
       const int c0 = static_cast<int>(u - static_cast<uint32_t>(t) * kc);
       const int c1 = static_cast<int>(cend - static_cast<uint32_t>(t) * kc);
       int g_base = 0;
+      float acc[FS ? NT : 1];  // FS: this set's part of the segment's sum
+#pragma unroll
+      for (int m = 0; m < (FS ? NT : 1); ++m) acc[m] = 0.f;
       for (int c = c0; c < c1; ++c, wp.advance(NW), rp.advance(NR), sel = (sel + 1 == NDS) ? 0 : sel + 1) {
         if (((c - c0) & box_mask) == 0) {
           if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));  // leaving box
@@ -578,8 +680,8 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         const auto zop = [&](int g) {
           return zero_operand<BF16>(*reinterpret_cast<const uint16_t*>(zs + (gi0 + g) * 256 + row * 2));
         };
-        // this set's TMEM slot was last read by the MMA of chunk i - NDS
-        if (mine > 0 && !(TM_DIAG & 1024)) mbar_wait(bar_done + 8 * rp_prev.slot, rp_prev.phase);
+        // this set's TMEM slot was last read by the MMA of chunk i - NDS (FS: waited below already)
+        if (!FS && mine > 0 && !(TM_DIAG & 1024)) mbar_wait(bar_done + 8 * rp_prev.slot, rp_prev.phase);
         rp_prev = rp;
         if (!(TM_DIAG & 8192)) tc_fence_after();
         const long long q2 = DCLK();
@@ -628,6 +730,33 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         mbar_arrive(bar_ready + 8 * r);
         if (lane == 0 && quarter == 0) DMARK(3);  // last chunk's operands written (latest wins)
         ++mine;
+        if constexpr (FS) {
+          // fused scale: once this chunk's MMAs completed, C += s_g * D_g for its groups (the D
+          // region and the operand slot are then free for the set's next chunk)
+          mbar_wait(bar_done + 8 * r, rp.phase);
+          tc_fence_after();
+          const uint8_t* ss = zs - Cfg::SZ_BOX;
+          const auto scale_of = [&](int g) {
+            return __half2float(__ushort_as_half(*reinterpret_cast<const uint16_t*>(ss + (gi0 + g) * 256 + row * 2)));
+          };
+          const uint32_t d_row = tmem_d0 + set * DSTRIDE + lane_off;
+          if (nb == Cfg::BLOBS) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(d_row, v);
+            const float s0 = scale_of(0), s1 = scale_of(1);
+            tc_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[j % NT] = fmaf(j < NT ? s0 : s1, __uint_as_float(v[j]), acc[j % NT]);
+          } else {  // K tail: one group
+            uint32_t v[16];
+            tmem_ld_32x32b_x16(d_row, v);
+            const float s0 = scale_of(0);
+            tc_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] = fmaf(s0, __uint_as_float(v[j]), acc[j]);
+          }
+          tc_fence_before();
+        }
         if (warp == Cfg::W_DEQ && lane == 0) {
           DACC(143, q1 - q0);
           DACC(144, q2 - q1);
@@ -636,6 +765,25 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
           DACC(159, q3 - q2);
           DACC(149, q4 - q3);
         }
+      }
+      if constexpr (FS) {
+        // segment end: sets 1..NDS-1 deposit their parts, set 0 adds them in set order
+        // (deterministic) and finishes the segment; the second barrier frees the deposit area
+        if (set > 0) {
+          float* dep = dep_ptr0 + (set - 1) * NT * 128 + row;
+#pragma unroll
+          for (int m = 0; m < NT; ++m) dep[m * 128] = acc[m];
+        }
+        asm volatile("bar.sync 3, %0;" ::"r"(128 * NDS) : "memory");
+        if (set == 0) {
+          for (int q = 1; q < NDS; ++q) {
+            const float* dep = dep_ptr0 + (q - 1) * NT * 128 + row;
+#pragma unroll
+            for (int m = 0; m < NT; ++m) acc[m] += dep[m * 128];
+          }
+          seg_end(acc, t, u, cend, row, row);
+        }
+        asm volatile("bar.sync 4, %0;" ::"r"(128 * NDS) : "memory");
       }
     }
     if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));
@@ -721,74 +869,63 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         rps.advance(NR);
       }
       if (et == 0) DMARK(4);  // accumulation of this segment finished (latest segment wins)
-      // ---- segment end.  A CTA's range [u0, u1) meets a shared tile only at its two ends: its
-      // first segment may be the tile's tail (or a middle piece), its last segment the tile's
-      // head.  The tail is computed first in time (start of the contributor's range), the head
-      // last (end of the head holder's range), so the head holder finalises: it waits for the
-      // contributors' flags (long set by then), adds their partials in fixed CTA order
-      // (deterministic) and stores.  A tail only stores its partial and raises its flag.
-      const long long qe = DCLK();
-      const uint32_t tile_lo = static_cast<uint32_t>(t) * kc;
-      const uint32_t tile_hi = tile_lo + kc;
-      const int n = nt * 128 + row;
-      const int mb = mt * NT;
-      const int mcount = (args.M - mb) < NT ? (args.M - mb) : NT;
-      if (CS > 1) {
-        // cluster split: reduced through distributed shared memory after the CTA-wide sync
-#pragma unroll
-        for (int m = 0; m < NT; ++m) acc_keep[m] = acc[m];
-      } else if (u != tile_lo) {
-        // tail / middle piece: always this CTA's first segment -> partial slot p, flag p
-        float* ws = args.workspace + static_cast<size_t>(p) * NT * 128;
-#pragma unroll
-        for (int m = 0; m < NT; ++m) __stcg(ws + m * 128 + row, acc[m]);
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (et == 0) st_release_gpu(args.counters + p, 1);  // cumulative over the barrier
-      } else {
-        if (cend != tile_hi) {
-          // head of a shared tile (this CTA's last segment): add the later contributors' partials
-          const int p_hi = dec_owner(tile_hi - 1, T, P);
-          if (et == 0)
-            for (int q = p + 1; q <= p_hi; ++q)
-              for (uint32_t spins = 0; ld_acquire_gpu(args.counters + q) == 0;)
-                if (++spins == (1u << 24)) __trap();  // a contributor never arrived: fail, do not hang
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          for (int q = p + 1; q <= p_hi; ++q) {  // fixed k order: deterministic
-            const float* wq = args.workspace + static_cast<size_t>(q) * NT * 128;
-#pragma unroll
-            for (int m = 0; m < NT; ++m) acc[m] += __ldcg(wq + m * 128 + row);
-          }
-          if (et == 0)
-            for (int q = p + 1; q <= p_hi; ++q) args.counters[q] = 0;  // consumed: zero for the next launch
-        }
-#pragma unroll
-        for (int m = 0; m < NT; ++m)
-          if (m < mcount) dec_store<BF16, OUT>(args.out, args.N, mb + m, n, acc[m]);
-      }
-      if (et == 0) DACC(157, DCLK() - qe);
+      seg_end(acc, t, u, cend, row, et);
     }
     if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));
   }
 
   if (warp == Cfg::W_SCALE && lane == 0) DMARK(5);  // epilogue finished
+  if (lane == 0 && warp < 20) DMARK(12 + warp);     // this warp's role finished
 #if TM_PROFILE
   if (args.trace) {
-    if (threadIdx.x == 0) {
-      uint64_t gt;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-      args.trace[blockIdx.x * 160 + 6] = static_cast<uint32_t>(gt);
-    }
     for (int k = 0; k < 24; ++k)
       if (prof[k]) atomicAdd(args.trace + blockIdx.x * 160 + 136 + k, prof[k]);
   }
 #endif
+  if (TM_CLUSTER_V2 && CS > 1) {
+    // ---- cluster split-K reduction, v2: as soon as its own partial is final, rank r > 0 parks it
+    // in its own (idle) weight ring and arrives on the leader's bar_red; the leader waits there,
+    // reads the partials through DSMEM in rank order (deterministic), adds and stores.  A final
+    // cluster barrier keeps ranks > 0 resident until the leader has read them.
+    cluster_wait();  // pairs the setup arrive
+    const uint32_t rank = cluster_ctarank();
+    if (warp >= Cfg::W_SCALE && warp < Cfg::W_SCALE + 4) {
+      const int row = (warp & 3) * 32 + static_cast<int>(lane);
+      if (rank > 0) {
+        float* mine = reinterpret_cast<float*>(base_ptr + Cfg::HDR);
+#pragma unroll
+        for (int m = 0; m < NT; ++m) mine[m * 128 + row] = acc_keep[m];
+        mbar_arrive_remote(mapa_shared(bar_red, 0));
+      } else {
+        mbar_wait_cluster(bar_red, 0);
+        if (threadIdx.x == Cfg::W_SCALE * 32) DMARK(34);
+        for (int q = 1; q < CS; ++q) {
+          const uint32_t src = mapa_shared(w0 + row * 4, static_cast<uint32_t>(q));
+#pragma unroll
+          for (int m = 0; m < NT; ++m) acc_keep[m] += ld_cluster_f32(src + m * 128 * 4);
+        }
+        const int t = p / CS;
+        const int n = (t % args.n_tiles) * 128 + row;
+        const int mb = (t / args.n_tiles) * NT;
+        const int mcount = (args.M - mb) < NT ? (args.M - mb) : NT;
+#pragma unroll
+        for (int m = 0; m < NT; ++m)
+          if (m < mcount) dec_store<BF16, OUT>(args.out, args.N, mb + m, n, acc_keep[m]);
+      }
+    }
+  }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) DMARK(32);  // every role finished
   if (warp == Cfg::W_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if (lane == 0) DMARK(33);
   }
-  if (CS > 1) {
+  if (TM_CLUSTER_V2 && CS > 1) {
+    cluster_arrive();
+    cluster_wait();
+  } else if (CS > 1) {
     // ---- cluster split-K reduction (DSMEM): ranks 1..CS-1 write their fp32 partials into the
     // leader's (now idle) weight ring, the leader adds them in rank order (deterministic) and
     // stores.  Barrier 1: every CTA is done with its rings; barrier 2: partials landed.
@@ -797,6 +934,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
     const int row = (warp & 3) * 32 + static_cast<int>(lane);
     cluster_arrive();
     cluster_wait();
+    if (threadIdx.x == 0) DMARK(34);
     if (scale && rank > 0) {
       const uint32_t dst = mapa_shared(w0 + ((rank - 1) * NT * 128 + row) * 4, 0);
 #pragma unroll
@@ -804,6 +942,7 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
     }
     cluster_arrive();
     cluster_wait();
+    if (threadIdx.x == 0) DMARK(35);
     if (scale && rank == 0) {
       const float* red = reinterpret_cast<const float*>(w_ptr0);
       for (int q = 1; q < CS; ++q) {
@@ -819,6 +958,15 @@ __global__ void __launch_bounds__(DecCfg<NT>::THREADS, 1)
         if (m < mcount) dec_store<BF16, OUT>(args.out, args.N, mb + m, n, acc_keep[m]);
     }
   }
+#if TM_PROFILE
+  // CTA end (slot 6): after the teardown and the cluster reduction, once every warp is done
+  __syncthreads();
+  if (args.trace && threadIdx.x == 0) {
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    args.trace[blockIdx.x * 160 + 6] = static_cast<uint32_t>(gt);
+  }
+#endif
 }
 
 #undef DEC_FOR_SEGMENTS
