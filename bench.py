@@ -227,6 +227,39 @@ def per_shape_detail(layers, io, ms, reps=20):
     return out
 
 
+def prefill_leg(stream, steps=5, M=8192):
+    """Secondary (tensor-bound) leg: the four Llama-3-8B layer GEMMs at M = 8192 tokens (BASELINE
+    configs[2]), one synthetic layer, graph-timed like the main leg; reported against the dense
+    bf16 tensor peak.  Not part of `value`."""
+    import torch
+    from paper_2508_15601_b200 import api, synth
+    calls, flops = [], 0
+    keep = []
+    for name, N, K in SHAPES:
+        d = synth.awq_like_torch(1, N, K, seed=7)
+        p = api.pack_w4(d["q"], d["s"], d["z"], 128)
+        A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        keep.append((p, d["s"], d["z"], A, C))
+        calls.append(lambda p=p, s=d["s"], z=d["z"], A=A, C=C: api.gemm_w4a16(A, p, s, z, out=C))
+        flops += 2 * M * N * K
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            for c in calls:
+                c()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for c in calls:
+                c()
+        g.replay()
+        torch.cuda.synchronize()
+        t = time_graph(g, steps, stream) / steps
+    del keep, g
+    torch.cuda.empty_cache()
+    return t, flops
+
+
 def ncu_traffic(ms, L):
     """Per-launch DRAM traffic of the GEMM kernel from the committed ncu capture, if present."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -370,6 +403,15 @@ def bench_ours(args):
     )
     clk = clk.summary()
     res["clocks"] = clk
+    if world == 1 and not args.no_prefill:
+        tp, fl = prefill_leg(stream)
+        achieved = fl / tp / 1e12
+        res["prefill"] = dict(
+            workload="Llama-3-8B prefill GEMMs (qkv/o/gate_up/down) at M=8192, group 128, bf16 (BASELINE configs[2])",
+            us_per_step=round(tp * 1e6, 1), tflops=round(achieved, 1),
+            roofline=dict(bound="tensor", achieved=round(achieved, 1), peak=peaks["tc"], unit="TFLOP/s",
+                          frac=round(achieved / peaks["tc"], 4),
+                          peak_source=f"MEASURED_PEAKS.json bf16_tflops ({peaks['src']}, burst: cuBLAS bf16 8192^3)"))
     if world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline()
     print(json.dumps(res), flush=True)
@@ -431,6 +473,7 @@ def main():
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--ms", default="1,8,16")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the secondary M=8192 tensor-bound leg")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

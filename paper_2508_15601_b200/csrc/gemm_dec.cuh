@@ -36,6 +36,13 @@
 //                           dequant
 // Per chunk: one full wait and one ready arrive (dequant), one ready wait + one D-slot wait +
 // one commit (MMA), one done wait + one D-slot release (scale).
+//
+// FS variant (cluster split-K, group 128): no scale warps.  Dequant set j waits for
+// the completion of its own chunk's MMAs, reads that chunk's D_g from its 32-column TMEM region
+// and accumulates s * D_g in registers; at the segment end sets 1..NDS-1 deposit their partial
+// sums in shared memory and set 0 adds them in set order (deterministic).
+// Operands go to TMEM as two 16-column tcgen05.st halves per blob, each issued as soon as its 4
+// words are dequantised (staging the operand is the largest single cost).
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -50,6 +57,12 @@ namespace w4k {
 
 #ifndef TM_CLUSTER_V2
 #define TM_CLUSTER_V2 0
+#endif
+#ifndef TM_ST_HALF
+#define TM_ST_HALF 1
+#endif
+#ifndef TM_PRE_BLOB
+#define TM_PRE_BLOB 1
 #endif
 #ifndef TM_EARLY_W
 #define TM_EARLY_W 0
@@ -680,16 +693,17 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
         const auto zop = [&](int g) {
           return zero_operand<BF16>(*reinterpret_cast<const uint16_t*>(zs + (gi0 + g) * 256 + row * 2));
         };
-        // this set's TMEM slot was last read by the MMA of chunk i - NDS (FS: waited below already)
-        if (!FS && mine > 0 && !(TM_DIAG & 1024)) mbar_wait(bar_done + 8 * rp_prev.slot, rp_prev.phase);
-        rp_prev = rp;
-        if (!(TM_DIAG & 8192)) tc_fence_after();
+        // this set's TMEM slot was last read by the MMA of chunk i - NDS (FS: waited at the end of
+        // the set's previous chunk already)
+        const auto wait_slot = [&]() {
+          if (!FS && mine > 0 && !(TM_DIAG & 1024)) mbar_wait(bar_done + 8 * rp_prev.slot, rp_prev.phase);
+          if (!(TM_DIAG & 8192)) tc_fence_after();
+        };
         const long long q2 = DCLK();
         // one blob: 8 LAYOUT v1 words (two LDS.128) -> 32 operand registers -> tcgen05.st x32
-        const auto blob_to_tmem = [&](int bb, uint32_t z2) {
+        const auto blob_regs = [&](int bb, uint32_t z2, uint32_t (&rr)[32]) {
           const uint4 xa = *reinterpret_cast<const uint4*>(wst + bb * 4096);
           const uint4 xb = *reinterpret_cast<const uint4*>(wst + bb * 4096 + 2048);
-          uint32_t rr[32];
           if (TM_DIAG & 2) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) rr[j] = (j & 1 ? xa.x : xb.y) + j;
@@ -703,25 +717,64 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
             deq_word_int<BF16>(xb.z, z2, rr + 24);
             deq_word_int<BF16>(xb.w, z2, rr + 28);
           }
+        };
+        const auto blob_st = [&](int bb, const uint32_t (&rr)[32]) {
           if ((TM_DIAG & 16) || ((TM_DIAG & 64) && bb >= 2))
             keep_alive_32(rr);
           else
             tmem_st_32x32b_x32(a_slot + bb * 32, rr);
         };
+        const auto blob_to_tmem = [&](int bb, uint32_t z2) {
+          if (TM_ST_HALF && !(TM_DIAG & (2 | 16 | 64))) {
+            // two halves (16 k-pairs each): the second half's LDS + math overlaps the first store
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint4 x = *reinterpret_cast<const uint4*>(wst + bb * 4096 + h * 2048);
+              uint32_t rr[16];
+              deq_word_int<BF16>(x.x, z2, rr + 0);
+              deq_word_int<BF16>(x.y, z2, rr + 4);
+              if (TM_ST_HALF == 2) tmem_st_32x32b_x8(a_slot + bb * 32 + h * 16, rr);
+              deq_word_int<BF16>(x.z, z2, rr + 8);
+              deq_word_int<BF16>(x.w, z2, rr + 12);
+              if (TM_ST_HALF == 2)
+                tmem_st_32x32b_x8(a_slot + bb * 32 + h * 16 + 8, rr + 8);
+              else
+                tmem_st_32x32b_x16(a_slot + bb * 32 + h * 16, rr);
+            }
+          } else {
+            uint32_t rr[32];
+            blob_regs(bb, z2, rr);
+            blob_st(bb, rr);
+          }
+        };
         if (nb == Cfg::BLOBS && bpg == 2) {  // full chunk, g = 128 (straight-line)
           const uint32_t z0 = zop(0), z1 = zop(1);
-          blob_to_tmem(0, z0);
+          // the first blob's operands are computed before the slot wait: the set's previous MMA
+          // is still completing (measured ~400 cycles of slot wait per owned chunk)
+          uint32_t r0[32];
+          if (TM_PRE_BLOB) blob_regs(0, z0, r0);
+          wait_slot();
+          if (!TM_PRE_BLOB) blob_regs(0, z0, r0);
+          if (TM_ST_HALF && !(TM_DIAG & (2 | 16 | 64))) {
+            tmem_st_32x32b_x16(a_slot, r0);
+            tmem_st_32x32b_x16(a_slot + 16, r0 + 16);
+          } else {
+            blob_st(0, r0);
+          }
           blob_to_tmem(1, z0);
           blob_to_tmem(2, z1);
           blob_to_tmem(3, z1);
         } else if (nb == Cfg::BLOBS) {      // full chunk, g = 64
+          wait_slot();
           blob_to_tmem(0, zop(0));
           blob_to_tmem(1, zop(1));
           blob_to_tmem(2, zop(2));
           blob_to_tmem(3, zop(3));
         } else {                            // K tail
+          wait_slot();
           for (int bb = 0; bb < nb; ++bb) blob_to_tmem(bb, zop(bb >> bshift));
         }
+        rp_prev = rp;
         const long long q3 = DCLK();
         mbar_arrive(bar_emptyw + 8 * ws);  // all LDS of the chunk's codes have completed
         if (!(TM_DIAG & 8192)) tc_wait_st();

@@ -89,6 +89,17 @@ def test_llama3_8b_decode_full(M, N, K):
     _assert_parity(C, d, tag=(M, N, K))
 
 
+@pytest.mark.parametrize("M", [100, 128, 200, 256, 512])
+@pytest.mark.parametrize("N,K", [(6144, 4096), (4096, 4096), (4096, 14336)])
+def test_llama3_8b_mid_m_split_configs(M, N, K):
+    """Mid M (65..512): the auto configuration splits K over a cluster of 2-4 CTAs per tile
+    (api.cu choose_config); full fp64 oracle on every row."""
+    cfg = api.query_gemm_config(M, N, K)
+    d = synth.awq_like(M, N, K, group=128, seed=1003 + M)
+    C, _, _ = _run(d)
+    _assert_parity(C, d, tag=(M, N, K, cfg))
+
+
 @pytest.mark.parametrize("N,K", [(6144, 4096), (28672, 4096), (4096, 14336)])
 def test_llama3_8b_prefill_sampled_rows(N, K):
     """CFG#2 (M=2048): sampled rows (first, last, tile boundaries, random) vs the oracle."""
