@@ -285,6 +285,32 @@ def test_decode_cluster_split_ragged(cs, group):
         api.set_decode_cluster(0)
 
 
+@pytest.mark.parametrize("group", [64, 128])
+def test_decode_one_cta_per_tile_ragged(group):
+    """Decode kernel with one CTA per tile and no split (forced; chosen automatically when
+    70-100 % of the SMs get a whole tile): all three tile sizes, ragged M, K tails."""
+    api.set_decode_cluster(-1)
+    try:
+        for M, N, K in ((1, 384, 896), (16, 256, 2048), (19, 512, 640), (33, 384, 1408), (64, 256, 4096)):
+            d = synth.awq_like(M, N, K, group=group, seed=M * 13 + N + K)
+            cfg = api.query_gemm_config(M, N, K)
+            assert cfg["kind"] == 2 and cfg["split_k"] == 1, cfg
+            C, _, _ = _run(d)
+            _assert_parity(C, d, tag=(M, N, K))
+    finally:
+        api.set_decode_cluster(0)
+
+
+@pytest.mark.parametrize("M", [1, 16, 40, 64])
+def test_mixtral_expert_auto_one_cta_per_tile(M):
+    """Mixtral expert (N=14336, K=4096; 112 tiles): the automatic choice is one CTA per tile."""
+    d = synth.awq_like(M, 14336, 4096, group=128, seed=1004 + M)
+    cfg = api.query_gemm_config(M, 14336, 4096)
+    assert cfg["kind"] == 2 and cfg["split_k"] == 1, cfg
+    C, _, _ = _run(d)
+    _assert_parity(C, d, tag=(M, cfg))
+
+
 def test_decode_cluster_auto_shapes_and_determinism():
     """Automatic choice on Llama-3-8B o_proj / qkv (cluster mode) is bit-stable run to run and
     within tolerance; partial f32 and fp16 variants."""

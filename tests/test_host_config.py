@@ -8,18 +8,21 @@ from paper_2508_15601_b200 import api
 
 SHAPES_8B = [(6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)]
 SHAPES_70B = [(10240, 8192), (8192, 8192), (57344, 8192), (8192, 28672)]
+MIXTRAL = [(14336, 4096)]
 SMS = 148
 
 
 @pytest.mark.parametrize("M", [1, 8, 16, 17, 32, 33, 64])
-@pytest.mark.parametrize("N,K", SHAPES_8B + SHAPES_70B)
+@pytest.mark.parametrize("N,K", SHAPES_8B + SHAPES_70B + MIXTRAL)
 def test_decode_configs_fit_one_wave(M, N, K):
     c = api.query_gemm_config(M, N, K)
     tiles = (N // 128) * ((M + c["tile_m"] - 1) // c["tile_m"])
     assert c["tile_m"] == (16 if M <= 16 else 32 if M <= 32 else 64)
     assert c["kind"] in (1, 2)
     assert c["grid_ctas"] <= SMS  # persistent / single wave
-    if c["kind"] == 2:  # cluster split-K: CS CTAs per tile, >= 8 chunks of 256 k each
+    if c["kind"] == 2 and c["split_k"] == 1:  # one CTA per tile: 70-100 % of the SMs busy
+        assert 0.7 * SMS <= tiles <= SMS and c["grid_ctas"] == tiles
+    elif c["kind"] == 2:  # cluster split-K: CS CTAs per tile, >= 8 chunks of 256 k each
         cs = c["split_k"]
         assert 2 <= cs <= 8 and c["grid_ctas"] == tiles * cs
         assert (K // 256) // cs >= 8
