@@ -137,8 +137,9 @@ struct DecCfg {
 // fits twice the ring of g = 64 (more slack between the MMA and the scale warps)
 template <int NT>
 __device__ __forceinline__ int dec_dring(int group) {
-  const int per_chunk = (256 / group) * NT;
-  const int n = DecCfg<NT>::DAVAIL / per_chunk;
+  // a chunk's D slots: (256 / group) * NT columns (compile-time per group: no runtime division)
+  constexpr int n64 = DecCfg<NT>::DAVAIL / (4 * NT), n128 = DecCfg<NT>::DAVAIL / (2 * NT);
+  const int n = group == 64 ? n64 : n128;
   return n >= 4 ? 4 : (n >= 2 ? 2 : 1);
 }
 // MMA issuers: two when each owns whole D ring entries and whole ready/done barriers (NA even:
@@ -317,9 +318,11 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
   const int CS = args.cluster;
   uint32_t u0, u1;
   if (CS > 0) {  // CS CTAs per tile: rank r takes chunks [r kc / CS, (r + 1) kc / CS) of tile p / CS
-    const uint32_t tl = static_cast<uint32_t>(p / CS) * args.kc, r = static_cast<uint32_t>(p % CS);
-    u0 = tl + (r * args.kc) / CS;
-    u1 = tl + ((r + 1) * args.kc) / CS;
+    // (unsigned 32-bit: a signed division is a called subroutine, an i-cache miss in the prologue)
+    const uint32_t ucs = static_cast<uint32_t>(CS), ukc = static_cast<uint32_t>(args.kc);
+    const uint32_t tile = static_cast<uint32_t>(p) / ucs, r = static_cast<uint32_t>(p) - tile * ucs;
+    u0 = tile * ukc + (r * ukc) / ucs;
+    u1 = tile * ukc + ((r + 1) * ukc) / ucs;
   } else {
     u0 = dec_start(p, T, P);
     u1 = dec_start(p + 1, T, P);
