@@ -754,10 +754,13 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
           const uint32_t z0 = zop(0), z1 = zop(1);
           // the first blob's operands are computed before the slot wait: the set's previous MMA
           // is still completing (measured ~400 cycles of slot wait per owned chunk)
+          // (FS: the slot is already free -- the set waited for its previous MMA -- so no early
+          // blob: it would only hold 32 more registers live)
+          constexpr bool pre = TM_PRE_BLOB && !FS;
           uint32_t r0[32];
-          if (TM_PRE_BLOB) blob_regs(0, z0, r0);
+          if (pre) blob_regs(0, z0, r0);
           wait_slot();
-          if (!TM_PRE_BLOB) blob_regs(0, z0, r0);
+          if (!pre) blob_regs(0, z0, r0);
           if (TM_ST_HALF && !(TM_DIAG & (2 | 16 | 64))) {
             tmem_st_32x32b_x16(a_slot, r0);
             tmem_st_32x32b_x16(a_slot + 16, r0 + 16);
