@@ -612,6 +612,8 @@ tm_status launch_sk(const void* A, const GemmArgs& g, const Config& c, cudaStrea
       if (g.group == 128 && c.kind == 2 && !no_fs) return launch_dec_t<16, BF16, OUT, true>(A, g, c, stream);
       return launch_dec_t<16, BF16, OUT, false>(A, g, c, stream);
     }
+    // (NT = 32/64 keep the scale warps: measured with the fused variant, NT = 32 cluster shapes
+    // were 6-13 % slower (2 dequant sets carry the scale work) and NT = 64 spills acc[64])
     case 32: return launch_dec_t<32, BF16, OUT, false>(A, g, c, stream);
     case 64: return launch_dec_t<64, BF16, OUT, false>(A, g, c, stream);
     case 128: return launch_sk_t<128, BF16, OUT>(A, g, c, stream);

@@ -119,8 +119,10 @@ struct DecCfg {
   static constexpr int MAX_CLUSTER = 1 + (NW * W_BYTES) / (NT * 512) < 8 ? 1 + (NW * W_BYTES) / (NT * 512) : 8;
   static constexpr int HDR = 1024;
   // FS: segment-end deposit of sets 1..NDS-1 (fp32 NT x 128 each)
-  static constexpr int DEP_BYTES = FS ? (NDS - 1) * NT * 128 * 4 : 0;
-  static constexpr int SMEM = 1024 + HDR + NW * W_BYTES + NA * ACT_BYTES + SZ_SLOTS * 2 * SZ_BOX + DEP_BYTES;
+  static constexpr int SMEM = 1024 + HDR + NW * W_BYTES + NA * ACT_BYTES + SZ_SLOTS * 2 * SZ_BOX;
+  // FS (cluster split-K only: one segment per CTA): the segment-end deposits of sets 1..NDS-1
+  // go to the weight ring, idle once every set has finished the CTA's chunks
+  static_assert(!FS || (NDS - 1) * NT * 128 * 4 <= NW * W_BYTES, "FS deposit area");
   static_assert(DAVAIL >= 4 * NT, "TMEM: one chunk of g = 64 D slots");
   static_assert(!FS || DAVAIL >= NDS * 2 * NT, "TMEM: FS D regions (group 128)");
   // a ready/done ring entry must be reused by the same dequant set (NA % NDS == 0: that set's
@@ -285,7 +287,7 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
   const uint32_t sz0 = a0 + NR * Cfg::ACT_BYTES;                // SZ_SLOTS x [s box | z box]
   const uint8_t* const w_ptr0 = base_ptr + Cfg::HDR;
   const uint8_t* const sz_ptr0 = w_ptr0 + NW * Cfg::W_BYTES + NR * Cfg::ACT_BYTES;
-  float* const dep_ptr0 = reinterpret_cast<float*>(const_cast<uint8_t*>(sz_ptr0) + Cfg::SZ_SLOTS * 2 * Cfg::SZ_BOX);
+  float* const dep_ptr0 = reinterpret_cast<float*>(base_ptr + Cfg::HDR);  // FS: the (idle) weight ring
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);  // warp-uniform
   const uint32_t lane = threadIdx.x & 31;
@@ -799,7 +801,20 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
             return __half2float(__ushort_as_half(*reinterpret_cast<const uint16_t*>(ss + (gi0 + g) * 256 + row * 2)));
           };
           const uint32_t d_row = tmem_d0 + set * DSTRIDE + lane_off;
-          if (nb == Cfg::BLOBS) {
+          if constexpr (NT >= 32) {
+            const int ng = nb >> 1;  // group 128: 2 blobs per group (K % 128 == 0)
+            for (int g = 0; g < ng; ++g) {
+              const float sg = scale_of(g);
+#pragma unroll
+              for (int m0 = 0; m0 < NT; m0 += 16) {  // 16-column loads: acc[NT] is live here
+                uint32_t v[16];
+                tmem_ld_32x32b_x16(d_row + g * NT + m0, v);
+                tc_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[m0 + j] = fmaf(sg, __uint_as_float(v[j]), acc[m0 + j]);
+              }
+            }
+          } else if (nb == Cfg::BLOBS) {
             uint32_t v[32];
             tmem_ld_32x32b_x32(d_row, v);
             const float s0 = scale_of(0), s1 = scale_of(1);
@@ -826,14 +841,16 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
         }
       }
       if constexpr (FS) {
-        // segment end: sets 1..NDS-1 deposit their parts, set 0 adds them in set order
-        // (deterministic) and finishes the segment; the second barrier frees the deposit area
+        // segment end (the CTA's only one: FS is cluster split-K): once every set is done with
+        // the weight ring, sets 1..NDS-1 deposit their parts there and set 0 adds them in set
+        // order (deterministic)
+        asm volatile("bar.sync 3, %0;" ::"r"(128 * NDS) : "memory");
         if (set > 0) {
           float* dep = dep_ptr0 + (set - 1) * NT * 128 + row;
 #pragma unroll
           for (int m = 0; m < NT; ++m) dep[m * 128] = acc[m];
         }
-        asm volatile("bar.sync 3, %0;" ::"r"(128 * NDS) : "memory");
+        asm volatile("bar.sync 4, %0;" ::"r"(128 * NDS) : "memory");
         if (set == 0) {
           for (int q = 1; q < NDS; ++q) {
             const float* dep = dep_ptr0 + (q - 1) * NT * 128 + row;
@@ -842,7 +859,6 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
           }
           seg_end(acc, t, u, cend, row, row);
         }
-        asm volatile("bar.sync 4, %0;" ::"r"(128 * NDS) : "memory");
       }
     }
     if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));
