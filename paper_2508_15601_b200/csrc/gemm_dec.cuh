@@ -55,8 +55,8 @@
 
 namespace w4k {
 
-#ifndef TM_CLUSTER_V2
-#define TM_CLUSTER_V2 0
+#ifndef TM_CLUSTER_PUSH
+#define TM_CLUSTER_PUSH 1
 #endif
 #ifndef TM_ST_HALF
 #define TM_ST_HALF 1
@@ -119,7 +119,11 @@ struct DecCfg {
   static constexpr int MAX_CLUSTER = 1 + (NW * W_BYTES) / (NT * 512) < 8 ? 1 + (NW * W_BYTES) / (NT * 512) : 8;
   static constexpr int HDR = 1024;
   // FS: segment-end deposit of sets 1..NDS-1 (fp32 NT x 128 each)
-  static constexpr int SMEM = 1024 + HDR + NW * W_BYTES + NA * ACT_BYTES + SZ_SLOTS * 2 * SZ_BOX;
+  // cluster split-K "push" reduction (NT = 16, CS <= 4): a dedicated landing area for the fp32
+  // partials of ranks 1..3, written through DSMEM as soon as each rank's sum is final
+  static constexpr int RED_MAX = (NT == 16 && FS) ? 3 : 0;  // (FS kernels are the cluster-mode ones)
+  static constexpr int RED_BYTES = RED_MAX * NT * 128 * 4;
+  static constexpr int SMEM = 1024 + HDR + NW * W_BYTES + NA * ACT_BYTES + SZ_SLOTS * 2 * SZ_BOX + RED_BYTES;
   // FS (cluster split-K only: one segment per CTA): the segment-end deposits of sets 1..NDS-1
   // go to the weight ring, idle once every set has finished the CTA's chunks
   static_assert(!FS || (NDS - 1) * NT * 128 * 4 <= NW * W_BYTES, "FS deposit area");
@@ -288,6 +292,7 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
   const uint8_t* const w_ptr0 = base_ptr + Cfg::HDR;
   const uint8_t* const sz_ptr0 = w_ptr0 + NW * Cfg::W_BYTES + NR * Cfg::ACT_BYTES;
   float* const dep_ptr0 = reinterpret_cast<float*>(base_ptr + Cfg::HDR);  // FS: the (idle) weight ring
+  const uint32_t red0 = sz0 + Cfg::SZ_SLOTS * 2 * Cfg::SZ_BOX;             // push reduction area
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);  // warp-uniform
   const uint32_t lane = threadIdx.x & 31;
@@ -318,6 +323,11 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
   const int p = blockIdx.x;
   const uint32_t T = static_cast<uint32_t>(args.total);
   const int CS = args.cluster;
+  // cluster split-K, push mode: every thread arrives on the cluster barrier in the setup and waits
+  // before its first remote access (or at its end), ranks > 0 push their partials into the
+  // leader's landing area and arrive on its bar_red, the leader waits there -- no cluster-wide
+  // barrier in the tail (vs two in the classic reduction)
+  const bool push = TM_CLUSTER_PUSH && Cfg::RED_MAX > 0 && CS > 1 && CS <= Cfg::RED_MAX + 1;
   uint32_t u0, u1;
   if (CS > 0) {  // CS CTAs per tile: rank r takes chunks [r kc / CS, (r + 1) kc / CS) of tile p / CS
     // (unsigned 32-bit: a signed division is a called subroutine, an i-cache miss in the prologue)
@@ -395,7 +405,7 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
       else cnt = 128 * NDS + (FS ? 0 : 128);                 // szempty
       mbar_init(bar_fullw + 8 * b, cnt);
     }
-    if (TM_CLUSTER_V2 && CS > 1 && lane == 0) mbar_init(bar_red, (CS - 1) * 128);
+    if (push && lane == 0) mbar_init(bar_red, (CS - 1) * 128);
     fence_mbar_init();
     __syncwarp();
     if (lane == 0) DMARK(7);
@@ -419,7 +429,8 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
   tc_fence_after();
   // cluster split: every thread arrives now and waits at its end, so the leader's bar_red is
   // initialised before any remote arrive without a cluster-wide stall in the setup
-  if (TM_CLUSTER_V2 && CS > 1) cluster_arrive_relaxed();
+  if (push) cluster_arrive_relaxed();
+  bool cl_waited = false;  // push mode: this thread has consumed its setup cluster arrive
   const uint32_t tmem_base = *tmem_slot_ptr;
   if (threadIdx.x == 0) DMARK(1);
   // PDL: let the next kernel in the stream start launching now; its CTAs take SMs as ours exit,
@@ -445,7 +456,27 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
     const int n = nt * 128 + row;
     const int mb = mt * NT;
     const int mcount = (args.M - mb) < NT ? (args.M - mb) : NT;
-    if (CS > 1) {
+    if (push) {
+      const uint32_t rank = cluster_ctarank();
+      cluster_wait();  // pairs the setup arrive: the leader's bar_red is initialised
+      cl_waited = true;
+      if (rank > 0) {
+        const uint32_t dst = mapa_shared(red0 + ((rank - 1) * NT * 128 + row) * 4, 0);
+#pragma unroll
+        for (int m = 0; m < NT; ++m) st_cluster_f32(dst + m * 128 * 4, acc[m]);
+        mbar_arrive_remote(mapa_shared(bar_red, 0));  // release: this thread's pushes first
+      } else {
+        mbar_wait_cluster(bar_red, 0);
+        const float* red = reinterpret_cast<const float*>(base_ptr + (red0 - base));
+        for (int q = 1; q < CS; ++q) {  // rank order: deterministic
+#pragma unroll
+          for (int m = 0; m < NT; ++m) acc[m] += red[(q - 1) * NT * 128 + m * 128 + row];
+        }
+#pragma unroll
+        for (int m = 0; m < NT; ++m)
+          if (m < mcount) dec_store<BF16, OUT>(args.out, args.N, mb + m, n, acc[m]);
+      }
+    } else if (CS > 1) {
       // cluster split: reduced through distributed shared memory after the CTA-wide sync
 #pragma unroll
       for (int m = 0; m < NT; ++m) acc_keep[m] = acc[m];
@@ -957,38 +988,6 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
       if (prof[k]) atomicAdd(args.trace + blockIdx.x * 160 + 136 + k, prof[k]);
   }
 #endif
-  if (TM_CLUSTER_V2 && CS > 1) {
-    // ---- cluster split-K reduction, v2: as soon as its own partial is final, rank r > 0 parks it
-    // in its own (idle) weight ring and arrives on the leader's bar_red; the leader waits there,
-    // reads the partials through DSMEM in rank order (deterministic), adds and stores.  A final
-    // cluster barrier keeps ranks > 0 resident until the leader has read them.
-    cluster_wait();  // pairs the setup arrive
-    const uint32_t rank = cluster_ctarank();
-    if (warp >= Cfg::W_SCALE && warp < Cfg::W_SCALE + 4) {
-      const int row = (warp & 3) * 32 + static_cast<int>(lane);
-      if (rank > 0) {
-        float* mine = reinterpret_cast<float*>(base_ptr + Cfg::HDR);
-#pragma unroll
-        for (int m = 0; m < NT; ++m) mine[m * 128 + row] = acc_keep[m];
-        mbar_arrive_remote(mapa_shared(bar_red, 0));
-      } else {
-        mbar_wait_cluster(bar_red, 0);
-        if (threadIdx.x == Cfg::W_SCALE * 32) DMARK(34);
-        for (int q = 1; q < CS; ++q) {
-          const uint32_t src = mapa_shared(w0 + row * 4, static_cast<uint32_t>(q));
-#pragma unroll
-          for (int m = 0; m < NT; ++m) acc_keep[m] += ld_cluster_f32(src + m * 128 * 4);
-        }
-        const int t = p / CS;
-        const int n = (t % args.n_tiles) * 128 + row;
-        const int mb = (t / args.n_tiles) * NT;
-        const int mcount = (args.M - mb) < NT ? (args.M - mb) : NT;
-#pragma unroll
-        for (int m = 0; m < NT; ++m)
-          if (m < mcount) dec_store<BF16, OUT>(args.out, args.N, mb + m, n, acc_keep[m]);
-      }
-    }
-  }
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) DMARK(32);  // every role finished
@@ -997,9 +996,8 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
     tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
     if (lane == 0) DMARK(33);
   }
-  if (TM_CLUSTER_V2 && CS > 1) {
-    cluster_arrive();
-    cluster_wait();
+  if (push) {
+    if (!cl_waited) cluster_wait();  // pairs the setup arrive (threads outside the reduction)
   } else if (CS > 1) {
     // ---- cluster split-K reduction (DSMEM): ranks 1..CS-1 write their fp32 partials into the
     // leader's (now idle) weight ring, the leader adds them in rank order (deterministic) and
