@@ -12,3 +12,4 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:w4a1
 timeout 300 python scripts/quick_perf.py --ms 2048,4096,8192 > gpurun_out/quick_perf_prefill.log 2>&1; echo "qp $?"
 timeout 300 python scripts/graph_perf.py --ms 1,8,16 --mix > gpurun_out/graph_perf.log 2>&1; echo "gp $?"
 timeout 300 python scripts/mid_sweep3.py > gpurun_out/mid_sweep.log 2>&1; echo "mid $?"
+for t in memcheck synccheck racecheck; do timeout 900 compute-sanitizer --tool $t --print-limit 20 python scripts/sanitize_cases.py > gpurun_out/sanitize_$t.log 2>&1; echo "$t $?"; tail -1 gpurun_out/sanitize_$t.log; done
