@@ -56,7 +56,7 @@
 namespace w4k {
 
 #ifndef TM_CLUSTER_PUSH
-#define TM_CLUSTER_PUSH 1
+#define TM_CLUSTER_PUSH 0
 #endif
 #ifndef TM_ST_HALF
 #define TM_ST_HALF 1
@@ -121,7 +121,7 @@ struct DecCfg {
   // FS: segment-end deposit of sets 1..NDS-1 (fp32 NT x 128 each)
   // cluster split-K "push" reduction (NT = 16, CS <= 4): a dedicated landing area for the fp32
   // partials of ranks 1..3, written through DSMEM as soon as each rank's sum is final
-  static constexpr int RED_MAX = (NT == 16 && FS) ? 3 : 0;  // (FS kernels are the cluster-mode ones)
+  static constexpr int RED_MAX = (TM_CLUSTER_PUSH && NT == 16 && FS) ? 3 : 0;  // (FS = the cluster-mode kernels)
   static constexpr int RED_BYTES = RED_MAX * NT * 128 * 4;
   static constexpr int SMEM = 1024 + HDR + NW * W_BYTES + NA * ACT_BYTES + SZ_SLOTS * 2 * SZ_BOX + RED_BYTES;
   // FS (cluster split-K only: one segment per CTA): the segment-end deposits of sets 1..NDS-1

@@ -22,7 +22,10 @@ cases = [  # (M, N, K, group, decode_cluster_force, (tile, split) override)
     (300, 384, 640, 64, 0, (256, 1)),   # tiled NT=256
 ]
 ok = True
-for M, N, K, g, force, (tile, split) in cases:
+only = os.environ.get("SAN_ONLY")
+for i, (M, N, K, g, force, (tile, split)) in enumerate(cases):
+    if only is not None and i != int(only):
+        continue
     api.set_decode_cluster(force)
     api.set_gemm_override(tile, split)
     d = synth.awq_like(M, N, K, group=g, seed=M + N + K)
