@@ -122,13 +122,16 @@ tm_status tm_set_gemm_override(int tile_m, int split_k);
 /* Launch configuration the next tm_gemm_* call with these sizes would use. */
 tm_status tm_query_gemm_config(int M, int N, int K, int* tile_m, int* split_k, int* grid_ctas);
 
-/* Which kernel that configuration runs: 0 = tiled (prefill), 1 = persistent stream-K decode,
- * 2 = decode with split_k CTAs per tile reduced in distributed shared memory over a
- * thread-block cluster (chosen when few output tiles would leave SMs idle).           */
+/* Which kernel that configuration runs: 0 = tiled (prefill; split_k > 1 = CTAs per tile along
+ * K in one cluster, chosen for 65 <= M <= 512 while tiles * split_k <= 128), 1 = persistent
+ * stream-K decode, 2 = decode with split_k CTAs per tile reduced in distributed shared memory
+ * over a thread-block cluster (chosen when few output tiles would leave SMs idle; split_k = 1:
+ * one CTA per tile, no split, when 70-100 % of the SMs get a whole tile).              */
 tm_status tm_query_gemm_kind(int M, int N, int K, int* kind);
 
 /* Decode cluster mode (tests / benchmarking only): 0 automatic (default), 1 never (always
- * stream-K), 2..8 force that many CTAs per tile (capped by shared memory and K).        */
+ * stream-K), 2..8 force that many CTAs per tile (capped by shared memory and K), -1 one CTA
+ * per tile without a split.                                                            */
 tm_status tm_set_decode_cluster(int cs);
 
 /* Debug timeline: when buf != NULL every GEMM CTA writes 160 uint32 events (clock cycles
