@@ -605,11 +605,10 @@ template <bool BF16, int OUT>
 tm_status launch_sk(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream) {
   switch (c.NT) {
     case 16: {
-      // group 128: dequant sets apply the group scales themselves (no scale warps)
-      static const bool no_fs = std::getenv("TM_NO_FS") != nullptr;  // experiments only
-      // (cluster split-K only: in stream-K mode the sets' segment-end barriers drain the pipeline
-      // mid-range -- measured gate_up M=16 17.4 -> 19.0 us -- while cluster CTAs have one segment)
-      if (g.group == 128 && c.kind == 2 && !no_fs) return launch_dec_t<16, BF16, OUT, true>(A, g, c, stream);
+      // fused-scale variant (dequant sets apply the group scales; cluster split-K, group 128):
+      // opt-in (TM_FS=1) -- measured 2.5 % slower on the bench mix in its final form
+      static const bool fs = std::getenv("TM_FS") != nullptr;
+      if (fs && g.group == 128 && c.kind == 2) return launch_dec_t<16, BF16, OUT, true>(A, g, c, stream);
       return launch_dec_t<16, BF16, OUT, false>(A, g, c, stream);
     }
     // (NT = 32/64 keep the scale warps: measured with the fused variant, NT = 32 cluster shapes

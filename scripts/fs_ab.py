@@ -1,5 +1,5 @@
 """FS (fused scale) vs scale warps for the cluster-mode decode shapes at M = 1..64 (graph-timed);
-set TM_NO_FS=1 in the environment for the B arm."""
+set TM_FS=1 in the environment for the fused-scale arm."""
 import os
 import sys
 
