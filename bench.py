@@ -203,8 +203,9 @@ def time_graph(graph, steps, stream):
     return e0.elapsed_time(e1) * 1e-3
 
 
-def per_shape_detail(layers, io, ms, reps=20):
-    """Eager per-(M, shape) timing outside the timed region (context; L2 rotates over layers)."""
+def per_shape_detail(layers, io, ms, reps=20, stream=None):
+    """Per-(M, shape) timing outside the timed region (context): CUDA-graph replay of `reps`
+    launches of one shape rotating over the L layers, like the main leg."""
     import torch
     from paper_2508_15601_b200 import api
     out = []
@@ -213,17 +214,22 @@ def per_shape_detail(layers, io, ms, reps=20):
             b = io[(M, name)]
             if layers[0][name]["kind"] == "row":
                 continue
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for r in range(reps):
-                w = layers[r % len(layers)][name]
-                api.gemm_w4a16(b["A"], w["packed"], w["s"], w["z"], out=b["C"])
-            e1.record()
-            torch.cuda.synchronize()
-            t = e0.elapsed_time(e1) * 1e-3 / reps
+            calls = [(lambda w=layers[r % len(layers)][name]: api.gemm_w4a16(b["A"], w["packed"], w["s"], w["z"],
+                                                                              out=b["C"])) for r in range(reps)]
+            with torch.cuda.stream(stream):
+                for c in calls:
+                    c()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    for c in calls:
+                        c()
+                g.replay()
+                torch.cuda.synchronize()
+                t = time_graph(g, 3, stream) / 3 / reps
             out.append(dict(M=M, shape=name, us=round(t * 1e6, 2), GBps=round(alg_bytes(M, N, K) / t / 1e9, 1),
                             cfg=api.query_gemm_config(M, N if layers[0][name]["kind"] == "full" else
-                                                      layers[0][name]["hi"] - layers[0][name]["lo"], K)))
+                                                      layers[0][name]["hi"] - layers[0][name]["lo"], K),
+                            timing="CUDA-graph replay, %d launches rotating over the layers" % reps))
     return out
 
 
@@ -376,8 +382,7 @@ def bench_ours(args):
     h2d = sum(io[(M, n)]["A"].numel() * 2 for M in ms for n, _, _ in SHAPES) * L
     d2h = sum(io[(M, n)]["C"].numel() * 2 for M in ms for n, _, _ in SHAPES) * L
     if world == 1:
-        with torch.cuda.stream(stream):  # same stream: reuses its stream-K workspace
-            detail = per_shape_detail(layers, io, ms)
+        detail = per_shape_detail(layers, io, ms, stream=stream)  # same stream: its stream-K workspace
     else:
         detail = None
     traffic = ncu_traffic(ms, L)
