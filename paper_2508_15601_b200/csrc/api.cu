@@ -322,6 +322,15 @@ int dec_max_cluster(int nt) {
   return 1;
 }
 
+// fewest 256-k chunks a cluster-split CTA may own (experiments: TM_DEC_MIN_CHUNKS)
+int dec_min_chunks() {
+  static const int v = [] {
+    const char* e = std::getenv("TM_DEC_MIN_CHUNKS");
+    return e ? std::atoi(e) : 8;
+  }();
+  return v;
+}
+
 Config choose_config(int M, int N, int K) {
   Config c{};
   int nt = 16;
@@ -369,7 +378,7 @@ Config choose_config(int M, int N, int K) {
       return c;
     } else if (force == 0) {
       for (int k = cmax; k >= 2; --k) {
-        if (k > kc || (kc + k - 1) / k < 8 || tiles * k > num_sms()) continue;
+        if (k > kc || (kc + k - 1) / k < dec_min_chunks() || tiles * k > num_sms()) continue;
         if (tiles > dec_active_clusters(nt, k)) continue;
         cs = k;
         break;
