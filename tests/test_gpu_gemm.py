@@ -89,6 +89,16 @@ def test_llama3_8b_decode_full(M, N, K):
     _assert_parity(C, d, tag=(M, N, K))
 
 
+@pytest.mark.parametrize("M", [1, 16])
+@pytest.mark.parametrize("N,K", [(57344, 8192), (8192, 28672), (59136, 8192), (8192, 29568)])
+def test_70b_qwen72b_decode_full(M, N, K):
+    """CFG#3/CFG#4 decode shapes at full size (Llama-3-70B gate_up/down, Qwen2-72B gate_up/down;
+    Qwen2-72B down K=29568 ends in a half chunk: the K-tail path at scale), full fp64 oracle."""
+    d = synth.awq_like(M, N, K, group=128, seed=1005 + M)
+    C, _, _ = _run(d)
+    _assert_parity(C, d, tag=(M, N, K, api.query_gemm_config(M, N, K)))
+
+
 @pytest.mark.parametrize("M", [100, 128, 200, 256, 512])
 @pytest.mark.parametrize("N,K", [(6144, 4096), (4096, 4096), (4096, 14336)])
 def test_llama3_8b_mid_m_split_configs(M, N, K):
