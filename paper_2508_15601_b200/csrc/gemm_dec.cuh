@@ -58,6 +58,12 @@ namespace w4k {
 #ifndef TM_CLUSTER_PUSH
 #define TM_CLUSTER_PUSH 0
 #endif
+#ifndef TM_NW16
+#define TM_NW16 6
+#endif
+#ifndef TM_NA16
+#define TM_NA16 6
+#endif
 #ifndef TM_ST_HALF
 #define TM_ST_HALF 1
 #endif
@@ -92,8 +98,8 @@ struct DecCfg {
   static constexpr int BLOBS = 4;                        // LAYOUT v1 blobs per chunk
   static constexpr int ACT_BYTES = NT * CH * 2;          // activation chunk (4 SW128 sub-tiles)
   static constexpr int W_BYTES = BLOBS * 4096;           // packed weight chunk
-  static constexpr int NW = NT <= 16 ? 8 : (NT <= 32 ? 6 : 5);   // weight ring (freed after the dequant's LDS)
-  static constexpr int NA = NT <= 32 ? 6 : 4;            // activation ring = per-chunk ready/done ring
+  static constexpr int NW = NT <= 16 ? TM_NW16 : (NT <= 32 ? 6 : 5);   // weight ring (freed after the dequant's LDS)
+  static constexpr int NA = NT <= 16 ? TM_NA16 : (NT <= 32 ? 6 : 4);   // activation ring = per-chunk ready/done ring
   static constexpr int NDS = NT <= 16 ? 3 : 2;           // dequant sets = TMEM operand slots
   static constexpr int DCOLS = NT;                       // one D_g slot
   static constexpr int DAVAIL = 512 - NDS * BLOBS * 32;  // TMEM columns left for the D ring
