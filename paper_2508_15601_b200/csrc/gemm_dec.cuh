@@ -58,6 +58,9 @@ namespace w4k {
 #ifndef TM_CLUSTER_PUSH
 #define TM_CLUSTER_PUSH 0
 #endif
+#ifndef TM_SZS
+#define TM_SZS 4
+#endif
 #ifndef TM_NW16
 #define TM_NW16 6
 #endif
@@ -119,7 +122,7 @@ struct DecCfg {
   static constexpr int W_DEQ = (FS || TM_SCALE_TOP) ? 4 : 8;               // 4 * NDS dequant warps
   static constexpr int SZG = 8;
   static constexpr int SZ_BOX = SZG * 128 * 2;
-  static constexpr int SZ_SLOTS = 4;                     // s/z boxes in flight (16 chunks of look-ahead)
+  static constexpr int SZ_SLOTS = TM_SZS;                // s/z boxes in flight (4: 16 chunks of look-ahead)
   static constexpr int TMEM_COLS = 512;
   // cluster split: the leader receives CS - 1 fp32 partials (NT x 128) in its weight ring
   static constexpr int MAX_CLUSTER = 1 + (NW * W_BYTES) / (NT * 512) < 8 ? 1 + (NW * W_BYTES) / (NT * 512) : 8;
