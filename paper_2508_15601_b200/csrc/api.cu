@@ -16,6 +16,7 @@
 #include "gemm_w4a16.cuh"
 #include "gemm_sk.cuh"
 #include "gemm_dec.cuh"
+#include "gemm_rf.cuh"
 
 namespace {
 
@@ -25,7 +26,12 @@ constexpr int kNumSMsDefault = 148;
 
 std::atomic<int> g_override_tile{0};
 std::atomic<int> g_override_split{0};
-std::atomic<int> g_dec_cluster{0};  // 0 automatic, 1 never (stream-K), 2..8 forced size,
+std::atomic<int> g_dec_cluster{0};
+// register-fed decode kernel for M <= 16 (1 = on, 0 = TMEM decode kernel); TM_RF=0 for A/B runs
+std::atomic<int> g_rf{[] {
+  const char* e = std::getenv("TM_RF");
+  return e ? std::atoi(e) : 0;
+}()};  // 0 automatic, 1 never (stream-K), 2..8 forced size,
                                      // -1 one CTA per tile (no split)
 uint32_t* g_trace = nullptr;  // debug timeline buffer (tm_set_trace)
 
@@ -177,9 +183,9 @@ tm_status act_tensor_map_3d(const void* A, int M, int K, int NT, int blobs, bool
   return TM_OK;
 }
 
-// 2-D map over s or z ([K/g][N] fp16): box {128 columns, 8 groups}.
-tm_status sz_tensor_map(const void* p, int G, int N, CUtensorMap* out) {
-  const MapKey key{p, G, N, 8 | (2 << 30), 2};
+// 2-D map over s or z ([K/g][N] fp16): box {128 columns, rows groups} (default 8).
+tm_status sz_tensor_map(const void* p, int G, int N, CUtensorMap* out, int rows = 8) {
+  const MapKey key{p, G, N, rows | (2 << 30), 2};
   {
     std::lock_guard<std::mutex> lk(g_map_mu);
     auto it = g_maps.find(key);
@@ -193,7 +199,7 @@ tm_status sz_tensor_map(const void* p, int G, int N, CUtensorMap* out) {
   CUtensorMap map;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(G)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(N) * 2};
-  const cuuint32_t box[2] = {128, 8};
+  const cuuint32_t box[2] = {128, static_cast<cuuint32_t>(rows)};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(p), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -350,8 +356,20 @@ Config choose_config(int M, int N, int K) {
   } else {
     nt = 256;
   }
-  c.NT = nt;
   const int n_tiles = N / 128;
+  if (ot <= 0 && g_override_split.load() == 0 && M <= 16 && g_rf.load()) {
+    // register-fed decode kernel (gemm_rf.cuh): persistent stream-K, one CTA per SM
+    c.kind = 3;
+    c.NT = M <= 8 ? 8 : 16;
+    const long long total = static_cast<long long>(n_tiles) * ((K + 255) / 256);
+    long long P = num_sms();
+    if (P > total) P = total;
+    c.split = static_cast<int>(P);
+    c.grid_x = c.split;
+    c.grid_y = 1;
+    return c;
+  }
+  c.NT = nt;
   const int m_tiles = (M + nt - 1) / nt;
   const int KS = K / 64;
   int split = 1;
@@ -610,8 +628,73 @@ tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaSt
   return TM_OK;
 }
 
+template <int NT, int GROUP, bool BF16, int OUT>
+tm_status launch_rf_t(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream) {
+  using Cfg = RfCfg<NT, TM_RF_NG>;
+  auto kern = w4a16_rf_kernel<NT, TM_RF_NG, GROUP, BF16, OUT>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return TM_ERR_CUDA;
+    }
+    configured = true;
+  }
+  CUtensorMap ma, ms, mz;
+  tm_status st = act_tensor_map_3d(A, g.M, g.K, NT, 4, BF16, &ma);
+  if (st != TM_OK) return st;
+  st = sz_tensor_map(g.scales, g.K / g.group, g.N, &ms, 256 / GROUP);
+  if (st != TM_OK) return st;
+  st = sz_tensor_map(g.zeros, g.K / g.group, g.N, &mz, 256 / GROUP);
+  if (st != TM_OK) return st;
+  RfArgs a;
+  a.trace = g_trace;
+  a.packed = g.packed;
+  a.scales = g.scales;
+  a.zeros = g.zeros;
+  a.out = g.out;
+  a.M = g.M;
+  a.N = g.N;
+  a.K = g.K;
+  a.group = g.group;
+  a.n_tiles = g.N / 128;
+  a.kc = (g.K + Cfg::CH - 1) / Cfg::CH;
+  const long long total = static_cast<long long>(a.n_tiles) * a.kc;
+  if (total * c.split >= (1ll << 32)) return TM_ERR_UNSUPPORTED_SHAPE;  // 32-bit range math
+  a.total = static_cast<uint32_t>(total);
+  st = get_workspace(stream, static_cast<size_t>(c.split) * NT * 128 * sizeof(float), c.split, &a.flags,
+                     &a.workspace);
+  if (st != TM_OK) return st;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(c.split, 1, 1);
+  cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, ms, mz, a);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return TM_ERR_CUDA;
+  }
+  return TM_OK;
+}
+
+template <int NT, bool BF16, int OUT>
+tm_status launch_rf_g(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream) {
+  if (g.group == 64) return launch_rf_t<NT, 64, BF16, OUT>(A, g, c, stream);
+  return launch_rf_t<NT, 128, BF16, OUT>(A, g, c, stream);
+}
+
 template <bool BF16, int OUT>
 tm_status launch_sk(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream) {
+  if (c.kind == 3) {
+    if (c.NT == 8) return launch_rf_g<8, BF16, OUT>(A, g, c, stream);
+    return launch_rf_g<16, BF16, OUT>(A, g, c, stream);
+  }
   switch (c.NT) {
     case 16: {
       // fused-scale variant (dequant sets apply the group scales; cluster split-K, group 128):
@@ -667,7 +750,7 @@ tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* sca
   args.split = c.split;
   args.trace = g_trace;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (c.kind == 1 || c.kind == 2) {
+  if (c.kind == 1 || c.kind == 2 || c.kind == 3) {
     if (out_kind == OUT_F32) return launch_sk<true, OUT_F32>(A, args, c, s);
     return bf16 ? launch_sk<true, OUT_ACT>(A, args, c, s) : launch_sk<false, OUT_ACT>(A, args, c, s);
   }

@@ -173,42 +173,6 @@ __device__ __forceinline__ uint32_t dec_start(uint32_t p, uint32_t T, uint32_t P
   return (p * T) / P;
 }
 
-#ifndef TM_DEQ_MULHI
-#define TM_DEQ_MULHI 0
-#endif
-// operand for the integer-exact MMA: x - (MAGIC + z) for the 4 pairs of one LAYOUT v1 word
-template <bool BF16>
-__device__ __forceinline__ void deq_word_int(uint32_t w, uint32_t z2, uint32_t* out) {
-  constexpr uint32_t MAGIC = BF16 ? 0x43004300u : 0x64006400u;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    // w >> 4i.  The dequant phase is ALU-pipe bound (3 SHF + 4 LOP3 = 14 ALU cycles per word vs
-    // 4 HSUB = 8 FMA cycles), so the last shift runs on the FMA pipe as mul.hi (half rate, 4
-    // cycles): 12 ALU / 12 FMA cycles per word.
-    uint32_t ws;
-    if (TM_DEQ_MULHI && i == 3)
-      asm("mul.hi.u32 %0, %1, %2;" : "=r"(ws) : "r"(w), "r"(1u << 20));
-    else
-      ws = w >> (4 * i);
-    uint32_t x;
-    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(x) : "r"(ws), "r"(0x000F000Fu), "r"(MAGIC));
-    uint32_t d;
-    if constexpr (BF16)
-      asm("sub.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(z2));
-    else
-      asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(z2));
-    out[i] = d;
-  }
-}
-
-template <bool BF16>
-__device__ __forceinline__ uint32_t zero_operand(uint16_t z_bits) {
-  const float zf = __half2float(__ushort_as_half(z_bits));
-  const uint16_t zb = BF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(128.0f + zf))
-                           : __half_as_ushort(__float2half_rn(1024.0f + zf));
-  return static_cast<uint32_t>(zb) | (static_cast<uint32_t>(zb) << 16);
-}
-
 template <bool BF16, int OUT>
 __device__ __forceinline__ void dec_store(void* out, int N, int m, int n, float x) {
   const size_t idx = static_cast<size_t>(m) * N + n;

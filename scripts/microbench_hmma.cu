@@ -1,0 +1,137 @@
+// Microbenchmark: legacy warp-level tensor path (mma.sync m16n8k16 bf16 -> f32, SASS HMMA) on
+// sm_100a, and a register-fed W4A16 decode inner loop built on it:
+//   mode 0: HMMA only, U independent accumulator chains per warp
+//   mode 1: LDS.128 of packed codes -> LOP3/SHF magic-number I2F (128+q) -> HMMA (NTOK tokens)
+//   mode 2: as 1 plus HSUB2 of (128+z) per pair (zero applied per weight)
+// Reports HMMA per clock per SM and weights per clock per SM (one CTA per SM, W warps).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+__device__ __forceinline__ void hmma(float* d, const uint32_t* a, const uint32_t* b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+__device__ __forceinline__ uint32_t lop3_mask_or(uint32_t x, uint32_t m, uint32_t o) {
+  uint32_t r;
+  asm volatile("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(r) : "r"(x), "r"(m), "r"(o));
+  return r;
+}
+
+template <int MODE, int U, int NTOK>
+__global__ void kern(int iters, unsigned long long* out, float* sink, uint32_t seed) {
+  extern __shared__ uint4 sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x)
+    sm[i] = make_uint4(seed * i, seed ^ i, i * 0x9E3779B9u, i + seed);
+  __syncthreads();
+  float acc[U][NTOK / 8][4];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int t = 0; t < NTOK / 8; ++t)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[u][t][e] = 0.f;
+  uint32_t b[NTOK / 8][2];
+#pragma unroll
+  for (int t = 0; t < NTOK / 8; ++t) {
+    b[t][0] = 0x3f803f80u ^ (lane << 3) ^ t;
+    b[t][1] = 0x3f003f00u ^ lane;
+  }
+  const uint32_t z2 = 0x43054305u;
+  const long long t0 = clock64();
+  if (MODE == 0) {
+    uint32_t a[4] = {seed, seed * 3, seed * 5, seed * 7};
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int t = 0; t < NTOK / 8; ++t) hmma(acc[u][t], a, b[t]);
+    }
+  } else {
+    // each iteration: one LDS.128 = 4 words = 4 A fragments (16x16 weights each)
+    uint32_t off = (warp * 32 + lane) & 4095;
+    for (int it = 0; it < iters; ++it) {
+      const uint4 v = sm[off];
+      off = (off + 128) & 4095;
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t a[4];
+        a[0] = lop3_mask_or(w[j], 0x000F000Fu, 0x43004300u);
+        a[1] = lop3_mask_or(w[j] >> 4, 0x000F000Fu, 0x43004300u);
+        a[2] = lop3_mask_or(w[j] >> 8, 0x000F000Fu, 0x43004300u);
+        a[3] = lop3_mask_or(w[j] >> 12, 0x000F000Fu, 0x43004300u);
+        if (MODE == 2) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&a[e]);
+            __nv_bfloat162 zz = *reinterpret_cast<const __nv_bfloat162*>(&z2);
+            x = __hsub2(x, zz);
+            a[e] = *reinterpret_cast<uint32_t*>(&x);
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < NTOK / 8; ++t) hmma(acc[j % U][t], a, b[t]);
+      }
+    }
+  }
+  const long long t1 = clock64();
+  if (lane == 0) out[blockIdx.x * 64 + warp] = t1 - t0;
+  float s = 0.f;
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int t = 0; t < NTOK / 8; ++t)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s += acc[u][t][e];
+  if (s == 1.2345f) sink[threadIdx.x] = s;
+}
+
+template <int MODE, int U, int NTOK>
+void run(int warps) {
+  unsigned long long* d;
+  float* sink;
+  cudaMalloc(&d, 148 * 64 * 8);
+  cudaMalloc(&sink, 4096);
+  const int iters = 4096;
+  cudaFuncSetAttribute(kern<MODE, U, NTOK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  kern<MODE, U, NTOK><<<148, 32 * warps, 65536>>>(iters, d, sink, 7);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  kern<MODE, U, NTOK><<<148, 32 * warps, 65536>>>(iters, d, sink, 7);
+  cudaEventRecord(e1);
+  cudaDeviceSynchronize();
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  unsigned long long h[64];
+  cudaMemcpy(h, d, 64 * 8, cudaMemcpyDeviceToHost);
+  double c = 0;
+  for (int i = 0; i < warps; ++i) c = c > h[i] ? c : h[i];
+  const double hmma_per_warp = (MODE == 0 ? (double)U * (NTOK / 8) : 4.0 * (NTOK / 8)) * iters;
+  const double hmma_per_clk_sm = hmma_per_warp * warps / c;
+  const double w_per_clk_sm = MODE == 0 ? 0 : 4.0 * 256 * iters * warps / c;
+  const double tbs = MODE == 0 ? 0 : 4.0 * 256 * iters * warps * 148 / 2.0 / (ms * 1e-3) / 1e12;
+  printf("mode %d U %d NTOK %2d warps %2d: cyc %.0f  HMMA/clk/SM %.3f  weights/clk/SM %.1f  (%.2f ms, "
+         "equiv %.2f TB/s of int4)  %s\n",
+         MODE, U, NTOK, warps, c, hmma_per_clk_sm, w_per_clk_sm, ms, tbs, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(d);
+  cudaFree(sink);
+}
+
+int main() {
+  for (int w : {4, 8, 16}) run<0, 4, 8>(w);
+  for (int w : {4, 8, 16}) run<0, 8, 16>(w);
+  for (int w : {4, 8, 16, 32}) run<1, 4, 8>(w);
+  for (int w : {4, 8, 16, 32}) run<1, 4, 16>(w);
+  for (int w : {4, 8, 16, 32}) run<2, 4, 16>(w);
+  return 0;
+}

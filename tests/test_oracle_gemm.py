@@ -104,11 +104,42 @@ def test_compare_metrics():
     z = np.full((1, 2), 15, dtype=np.float16)
     s = np.full((1, 2), 0.5, dtype=np.float16)
     A = np.ones((2, 128))
-    b_bf = compare.elem_bound(A, s, z, compare.max_weight_dev(q, z, 128), 128, "bf16")
-    b_h = compare.elem_bound(A, s, z, 0, 128, "fp16")
+    b_bf = compare.elem_bound(A, s, z, q, 128, "bf16")
+    b_h = compare.elem_bound(A, s, z, q, 128, "fp16")
     assert b_h == pytest.approx(1e-2 * 0.5) and b_bf == pytest.approx(15 * 1e-2 * 0.5)
     r = compare.check(C * (1 + 1e-3), C, A, q, s, z, 128, "fp16")
     assert r["relfro"] == pytest.approx(1e-3) and r["argmax"] == (1, 1)
+
+
+def test_compare_bound_is_max_dequant_weight_not_product_of_maxima():
+    """Reading R12: S = max|s*(q-z)| element by element.  Here the largest scale sits in a
+    group whose codes equal the zero (dequantised weight 0), and the largest |q-z| sits in a
+    group with a small scale, so max|s|*max|q-z| = 2*15 = 30 while max|s*(q-z)| = 0.25*15."""
+    K, N, g = 256, 128, 128
+    q = np.zeros((K, N), dtype=np.uint8)
+    z = np.zeros((K // g, N), dtype=np.float16)
+    s = np.full((K // g, N), 0.25, dtype=np.float16)
+    s[0, :] = 2.0                      # group 0: big scale, q == z -> weight 0
+    q[g:, :] = 15                      # group 1: |q - z| = 15 at scale 0.25
+    assert compare.max_dequant_weight(q, s, z, g) == 0.25 * 15
+    A = np.ones((1, K))
+    B = compare.elem_bound(A, s, z, q, g, "bf16")
+    assert B == pytest.approx(1e-2 * np.sqrt(2.0) * 0.25 * 15)
+    assert B < 1e-2 * np.sqrt(2.0) * 2.0 * 15 / 4          # the looser product reading is 8x larger
+    # an error between the two readings is rejected under R12
+    C_ref = np.zeros((1, N))
+    C_ref[0, :] = 15 * 0.25 * g
+    C = C_ref + 2.0 * B
+    r = compare.check(C, C_ref, A, q, s, z, g, "fp32")
+    assert not r["ok"] and r["max_ratio"] == pytest.approx(2.0) and r["max_ratio_strict"] == pytest.approx(2.0)
+    # fp16 reads the literal max|s|
+    assert compare.elem_bound(A, s, z, q, g, "fp16") == pytest.approx(1e-2 * np.sqrt(2.0) * 2.0)
+
+
+def test_max_dequant_weight_column_blocks():
+    d = synth.uniform(1, 384, 256, group=64, seed=5)
+    full = float(np.max(np.abs(dequant_f64(d["q"], d["s"], d["z"], 64))))
+    assert compare.max_dequant_weight(d["q"], d["s"], d["z"], 64, col_block=128) == full
 
 
 def test_compare_half_ulp_allowance():
@@ -123,6 +154,7 @@ def test_compare_half_ulp_allowance():
     A = np.full((4, 128), 1e-3)
     r = compare.check(round_bf16(C_ref), C_ref, A, q, s, z, 128, "bf16")
     assert r["max_ratio"] <= 1.0
+    assert r["max_ratio_strict"] > 1.0   # B alone (q == z: S = 0) would reject the exact answer
     # an error of one full ulp fails
     from oracle.numerics import ulp
     r = compare.check(C_ref + ulp(C_ref, "bf16"), C_ref, A, q, s, z, 128, "bf16")
