@@ -9,11 +9,14 @@ One step = every (M, layer, shape) GEMM once (48 launches at L = 4).
 
 value  = algorithmic bytes of the step (packed codes + fp16 s/z + A + C) / time,
          device-timed with CUDA events around a CUDA-graph replay of K steps, inputs resident.
-e2e    = same through the public API with each GEMM's A copied from pinned host memory and
-         C copied back to pinned host memory inside the timed region.
-N > 1  : tensor parallel (torchrun, one process per GPU, NCCL): qkv and gate_up column-parallel,
-         o and down row-parallel with an fp32 all-reduce + finalize; strong scaling of the same
-         workload; time = max over ranks.
+e2e    = same through the public API with the step's activations copied from pinned host memory
+         (one copy) and its outputs copied back (one copy) inside the timed region, on two copy
+         streams double-buffered against the compute graph.
+N > 1  : tensor parallel (torchrun, one process per GPU, NCCL; `--gpus N` alone self-launches
+         the N ranks): qkv and gate_up column-parallel, o and down row-parallel with an fp32
+         all-reduce + finalize (paper_2508_15601_b200/tp.py classes); the step, all-reduces
+         included, is one CUDA graph; strong scaling of the same workload; time = max over
+         ranks; GEMM and all-reduce times are reported separately under "tp".
 --impl reference: the CPU oracle (oracle/gemm.py, fp64) on a bounded sample of the workload.
 """
 
@@ -114,52 +117,64 @@ def dist_env():
 
 # ---------------------------------------------------------------------------------- our arm
 def build_layers(L, world, rank, device):
+    """L synthetic Llama-3-8B layers as the product's tensor-parallel layer classes
+    (paper_2508_15601_b200/tp.py): qkv/gate_up ColumnParallelW4, o/down RowParallelW4 at
+    world > 1; every layer ColumnParallelW4 over the whole N (one shard) at world = 1."""
     import torch
-    from paper_2508_15601_b200 import api, synth
-    from paper_2508_15601_b200.tp import shard_bounds
+    from paper_2508_15601_b200 import synth
+    from paper_2508_15601_b200.tp import ColumnParallelW4, RowParallelW4
     layers = []
     for li in range(L):
         lay = {}
         for name, N, K in SHAPES:
             d = synth.awq_like_torch(1, N, K, group=128, seed=7000 + 17 * li + N + K, device=device)
-            q, s, z = d["q"], d["s"], d["z"]
             if world > 1 and name in ROW_PARALLEL:
-                lo, hi = shard_bounds(K, world, rank, 128)
-                q, s, z = q[lo:hi].contiguous(), s[lo // 128:hi // 128].contiguous(), z[lo // 128:hi // 128].contiguous()
-                kind = "row"
-            elif world > 1:
-                lo, hi = shard_bounds(N, world, rank, 128)
-                q, s, z = q[:, lo:hi].contiguous(), s[:, lo:hi].contiguous(), z[:, lo:hi].contiguous()
-                kind = "col"
+                lay[name] = RowParallelW4(d["q"], d["s"], d["z"], 128, world, rank)
             else:
-                lo, hi, kind = 0, N, "full"
-            p = api.pack_w4(q, s, z, 128)
-            lay[name] = dict(packed=p, s=s, z=z, N=N, K=K, kind=kind, lo=lo, hi=hi)
-            del d, q
+                lay[name] = ColumnParallelW4(d["q"], d["s"], d["z"], 128, world if world > 1 else 1,
+                                             rank if world > 1 else 0)
+            del d
         layers.append(lay)
         torch.cuda.synchronize()
     return layers
 
 
-def make_io(layers, ms, device, world):
+def make_io(layers, ms, device, nsets=2):
+    """Per buffer set: every (M, shape)'s A and C as views into one contiguous device buffer
+    (so the end-to-end leg moves a step's inputs and outputs with one copy each way)."""
     import torch
-    io = {}
     g = torch.Generator(device=device)
     g.manual_seed(1234)
+    shapes = []
     for M in ms:
         for name, N, K in SHAPES:
             w = layers[0][name]
-            Kl = (w["hi"] - w["lo"]) if w["kind"] == "row" else K
-            Nl = (w["hi"] - w["lo"]) if w["kind"] == "col" else N
-            A = torch.randn(M, Kl, device=device, generator=g).to(torch.bfloat16)
-            C = torch.empty(M, Nl, device=device, dtype=torch.bfloat16)
-            P = torch.empty(M, N, device=device, dtype=torch.float32) if w["kind"] == "row" else None
+            row = hasattr(w, "local_partial")
+            Kl = (w.hi - w.lo) if row else K
+            Nl = N if row else (w.hi - w.lo)
+            shapes.append((M, name, Kl, Nl, row, N))
+    a_elems = sum(M * Kl for M, _, Kl, _, _, _ in shapes)
+    c_elems = sum(M * Nl for M, _, _, Nl, _, _ in shapes)
+    src = torch.randn(a_elems, device=device, generator=g).to(torch.bfloat16)
+    sets = []
+    for _ in range(nsets):
+        A_all = src.clone()
+        C_all = torch.empty(c_elems, device=device, dtype=torch.bfloat16)
+        io, ao, co = {}, 0, 0
+        for M, name, Kl, Nl, row, N in shapes:
+            A = A_all[ao:ao + M * Kl].view(M, Kl)
+            C = C_all[co:co + M * Nl].view(M, Nl)
+            P = torch.empty(M, N, device=device, dtype=torch.float32) if row else None
             io[(M, name)] = dict(A=A, C=C, P=P)
-    return io
+            ao += M * Kl
+            co += M * Nl
+        sets.append(dict(io=io, A_all=A_all, C_all=C_all))
+    return sets
 
 
-def run_step(layers, io, ms, e2e=None):
-    """One step: every (M, layer, shape) GEMM.  e2e: dict of pinned host buffers -> copies in."""
+def run_step(layers, io, ms, part="all"):
+    """One step: every (M, layer, shape) GEMM.  part: "all"; "gemm" (the local GEMMs and the
+    finalize of row-parallel layers, no collective); "comm" (only the all-reduces)."""
     from paper_2508_15601_b200 import api
     from paper_2508_15601_b200.tp import allreduce_sum_fp32
     n = 0
@@ -167,18 +182,18 @@ def run_step(layers, io, ms, e2e=None):
         for lay in layers:
             for name, N, K in SHAPES:
                 w, b = lay[name], io[(M, name)]
-                if e2e is not None:
-                    b["A"].copy_(e2e[(M, name)]["A"], non_blocking=True)
-                if w["kind"] == "row":
-                    api.gemm_w4a16_partial_f32(b["A"], w["packed"], w["s"], w["z"], out=b["P"])
-                    allreduce_sum_fp32(b["P"])
-                    api.tp_finalize(b["P"], out=b["C"])
-                    n += 2
-                else:
-                    api.gemm_w4a16(b["A"], w["packed"], w["s"], w["z"], out=b["C"])
+                if hasattr(w, "local_partial"):  # row-parallel: fp32 partial, all-reduce, finalize
+                    if part != "comm":
+                        w.local_partial(b["A"], out=b["P"])
+                        n += 1
+                    if part != "gemm":
+                        allreduce_sum_fp32(b["P"])
+                    if part != "comm":
+                        api.tp_finalize(b["P"], out=b["C"])
+                        n += 1
+                elif part != "comm":
+                    w(b["A"], out=b["C"])
                     n += 1
-                if e2e is not None:
-                    e2e[(M, name)]["C"].copy_(b["C"], non_blocking=True)
     return n
 
 
@@ -203,67 +218,73 @@ def time_graph(graph, steps, stream):
     return e0.elapsed_time(e1) * 1e-3
 
 
+def capture(fn, stream):
+    import torch
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+        g.replay()
+    torch.cuda.synchronize()
+    return g
+
+
 def per_shape_detail(layers, io, ms, reps=20, stream=None):
     """Per-(M, shape) timing outside the timed region (context): CUDA-graph replay of `reps`
     launches of one shape rotating over the L layers, like the main leg."""
-    import torch
     from paper_2508_15601_b200 import api
     out = []
     for M in ms:
         for name, N, K in SHAPES:
             b = io[(M, name)]
-            if layers[0][name]["kind"] == "row":
+            if hasattr(layers[0][name], "local_partial"):
                 continue
-            calls = [(lambda w=layers[r % len(layers)][name]: api.gemm_w4a16(b["A"], w["packed"], w["s"], w["z"],
-                                                                              out=b["C"])) for r in range(reps)]
-            with torch.cuda.stream(stream):
-                for c in calls:
-                    c()
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=stream):
-                    for c in calls:
-                        c()
-                g.replay()
-                torch.cuda.synchronize()
-                t = time_graph(g, 3, stream) / 3 / reps
-            out.append(dict(M=M, shape=name, us=round(t * 1e6, 2), GBps=round(alg_bytes(M, N, K) / t / 1e9, 1),
-                            cfg=api.query_gemm_config(M, N if layers[0][name]["kind"] == "full" else
-                                                      layers[0][name]["hi"] - layers[0][name]["lo"], K),
+            calls = [(lambda w=layers[r % len(layers)][name]: w(b["A"], out=b["C"])) for r in range(reps)]
+            g = capture(lambda: [c() for c in calls], stream)
+            t = time_graph(g, 3, stream) / 3 / reps
+            Nl = layers[0][name].hi - layers[0][name].lo
+            out.append(dict(M=M, shape=name, us=round(t * 1e6, 2), GBps=round(alg_bytes(M, Nl, K) / t / 1e9, 1),
+                            cfg=api.query_gemm_config(M, Nl, K),
                             timing="CUDA-graph replay, %d launches rotating over the layers" % reps))
     return out
 
 
-def prefill_leg(stream, steps=5, M=8192):
+def prefill_leg(stream, min_seconds=1.0, M=8192):
     """Secondary (tensor-bound) leg: the four Llama-3-8B layer GEMMs at M = 8192 tokens (BASELINE
-    configs[2]), one synthetic layer, graph-timed like the main leg; reported against the dense
-    bf16 tensor peak.  Not part of `value`."""
+    configs[2]), one synthetic layer, graph-timed like the main leg with the clocks sampled over
+    a timed region of >= min_seconds; reported against the dense bf16 tensor peak.  Not part
+    of `value`.  torch.matmul bf16 on the same shapes (the paper's E2 comparison)
+    is timed beside it."""
     import torch
     from paper_2508_15601_b200 import api, synth
-    calls, flops = [], 0
+    calls, dense, flops = [], [], 0
     keep = []
     for name, N, K in SHAPES:
         d = synth.awq_like_torch(1, N, K, seed=7)
         p = api.pack_w4(d["q"], d["s"], d["z"], 128)
         A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
         C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-        keep.append((p, d["s"], d["z"], A, C))
+        Wd = torch.randn(K, N, device="cuda").to(torch.bfloat16)
+        keep.append((p, d["s"], d["z"], A, C, Wd))
         calls.append(lambda p=p, s=d["s"], z=d["z"], A=A, C=C: api.gemm_w4a16(A, p, s, z, out=C))
+        dense.append(lambda A=A, Wd=Wd, C=C: torch.matmul(A, Wd, out=C))
         flops += 2 * M * N * K
     with torch.cuda.stream(stream):
         for _ in range(3):
-            for c in calls:
+            for c in calls + dense:
                 c()
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            for c in calls:
-                c()
-        g.replay()
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    g = capture(lambda: [c() for c in calls], stream)
+    gd = capture(lambda: [c() for c in dense], stream)
+    t1 = time_graph(g, 2, stream) / 2
+    steps = max(5, int(min_seconds / t1) + 1)
+    with ClockSampler(torch.cuda.current_device()) as clk:
         t = time_graph(g, steps, stream) / steps
-    del keep, g
+    td = time_graph(gd, max(5, int(min_seconds / 2 / t1) + 1), stream)
+    td /= max(5, int(min_seconds / 2 / t1) + 1)
+    del keep, g, gd
     torch.cuda.empty_cache()
-    return t, flops
+    return t, flops, steps, clk.summary(), td
 
 
 def ncu_traffic(ms, L):
@@ -300,14 +321,62 @@ def cpu_baseline(seconds_budget=20.0):
             break
     threads = max([x.get("num_threads", 1) for x in threadpool_info()] + [1])
     return dict(value=round(b_total / t_total / 1e9, 3), unit="GB/s", cores=threads, kind="oracle",
+                cpu_model=cpu_model(),
                 sample=f"oracle fp64 GEMM (dequant + numpy matmul) of one layer's {'/'.join(done)} at M=16; "
                        f"{t_total:.1f} s on host; os.cpu_count()={os.cpu_count()}")
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def time_e2e(graphs, sets, host_A, host_C, steps, comp):
+    """End to end through the public API: every step copies its inputs host -> device (one
+    pinned-memory copy of all the step's activations) and its outputs device -> host (one copy of
+    all the step's C), on two copy streams, double-buffered so step i's copies overlap step
+    i +- 1's GEMMs.  Timed with CUDA events from before the first input copy to after the last
+    output copy."""
+    import torch
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_comp = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(comp)
+    h2d.wait_event(e0)
+    for i in range(steps):
+        b = i % 2
+        if i >= 2:
+            h2d.wait_event(ev_comp[b])  # step i - 2 finished reading this input buffer
+        with torch.cuda.stream(h2d):
+            sets[b]["A_all"].copy_(host_A, non_blocking=True)
+        ev_in[b].record(h2d)
+        comp.wait_event(ev_in[b])
+        if i >= 2:
+            comp.wait_event(ev_out[b])  # step i - 2's outputs have left this buffer
+        graphs[b].replay()
+        ev_comp[b].record(comp)
+        d2h.wait_event(ev_comp[b])
+        with torch.cuda.stream(d2h):
+            host_C.copy_(sets[b]["C_all"], non_blocking=True)
+        ev_out[b].record(d2h)
+    comp.wait_stream(d2h)
+    e1.record(comp)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e-3
 
 
 def bench_ours(args):
     import torch
     import torch.distributed as dist
-    from paper_2508_15601_b200 import api
     world, rank, local = dist_env()
     if world > 1:
         dist.init_process_group("nccl", init_method="env://")
@@ -316,60 +385,46 @@ def bench_ours(args):
     ms = [int(x) for x in args.ms.split(",")]
     L = args.layers
     layers = build_layers(L, world, rank, device)
-    io = make_io(layers, ms, device, world)
-    # pinned host buffers for the e2e leg
-    host = {k: dict(A=v["A"].cpu().pin_memory(), C=torch.empty(v["C"].shape, dtype=v["C"].dtype).pin_memory())
-            for k, v in io.items()}
+    sets = make_io(layers, ms, device)
+    io = sets[0]["io"]
+    host_A = sets[0]["A_all"].cpu().pin_memory()
+    host_C = torch.empty(sets[0]["C_all"].numel(), dtype=torch.bfloat16).pin_memory()
     stream = torch.cuda.Stream(device)
     with torch.cuda.stream(stream):
         for _ in range(max(args.warmup, 3)):
             n_launch = run_step(layers, io, ms)
-        torch.cuda.synchronize()
-        use_graph = world == 1
-        if use_graph:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                run_step(layers, io, ms)
-            ge = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(ge, stream=stream):
-                run_step(layers, io, ms, e2e=host)
-            for _ in range(2):
-                g.replay()
-                ge.replay()
-            torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    # the whole step -- GEMMs and, under TP, the NCCL all-reduces -- is one CUDA graph
+    graphs = [capture(lambda st=st: run_step(layers, st["io"], ms), stream) for st in sets]
+    g = graphs[0]
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
     nbytes, nflops = step_bytes(ms, L)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        with torch.cuda.stream(stream):
-            if use_graph:
-                t = time_graph(g, args.steps, stream)
-            else:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                for _ in range(args.steps):
-                    run_step(layers, io, ms)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                t = e0.elapsed_time(e1) * 1e-3
+        t = time_graph(g, args.steps, stream)
     torch.cuda.synchronize()
-    # e2e (host copies in the timed region)
-    with torch.cuda.stream(stream):
-        if use_graph:
-            te = time_graph(ge, args.steps, stream)
-        else:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(args.steps):
-                run_step(layers, io, ms, e2e=host)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            te = e0.elapsed_time(e1) * 1e-3
+    te = time_e2e(graphs, sets, host_A, host_C, args.steps, stream)
+    tp_detail = None
     if world > 1:
-        tt = torch.tensor([t, te], device=device, dtype=torch.float64)
+        gg = capture(lambda: run_step(layers, io, ms, part="gemm"), stream)
+        gc = capture(lambda: run_step(layers, io, ms, part="comm"), stream)
+        dist.barrier()
+        t_gemm = time_graph(gg, args.steps, stream)
+        dist.barrier()
+        t_comm = time_graph(gc, args.steps, stream)
+        tt = torch.tensor([t, te, t_gemm, t_comm], device=device, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t, te = float(tt[0]), float(tt[1])
+        t, te, t_gemm, t_comm = (float(x) for x in tt)
+        ar_bytes = sum(M * N * 4 for M in ms for n, N, K in SHAPES if n in ROW_PARALLEL) * L
+        tp_detail = dict(
+            gemm_ms_per_step=round(t_gemm / args.steps * 1e3, 4), allreduce_ms_per_step=round(t_comm / args.steps * 1e3, 4),
+            allreduce_bytes_per_step=int(ar_bytes), allreduces_per_step=len(ms) * L * len(ROW_PARALLEL),
+            note="max over ranks of CUDA-graph replays of (a) only the local GEMMs + finalize and (b) only the "
+                 "fp32 NCCL all-reduces; the step graph (value) runs both in order")
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -379,14 +434,10 @@ def bench_ours(args):
     value = nbytes / per_step / 1e9
     e2e_value = nbytes / (te / args.steps) / 1e9
     peaks = load_peaks()
-    h2d = sum(io[(M, n)]["A"].numel() * 2 for M in ms for n, _, _ in SHAPES) * L
-    d2h = sum(io[(M, n)]["C"].numel() * 2 for M in ms for n, _, _ in SHAPES) * L
-    if world == 1:
-        detail = per_shape_detail(layers, io, ms, stream=stream)  # same stream: its stream-K workspace
-    else:
-        detail = None
+    h2d = host_A.numel() * 2
+    d2h = host_C.numel() * 2
+    detail = per_shape_detail(layers, io, ms, stream=stream) if world == 1 else None
     traffic = ncu_traffic(ms, L)
-    gemm_launches = len(ms) * L * len(SHAPES)
     res = dict(
         metric=METRIC, value=round(value, 1), unit="GB/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
         ms_per_step=round(per_step * 1e3, 4), higher_is_better=True, scaling="strong" if world > 1 else "weak",
@@ -396,24 +447,30 @@ def bench_ours(args):
                     weights_bytes_per_step=int(sum(K * N // 2 for _, N, K in SHAPES) * L * len(ms)),
                     l2_policy="inputs larger than L2: %d MB of packed weights per pass (> 3 x 126 MB L2)" %
                               (sum(K * N // 2 for _, N, K in SHAPES) * L // 2 ** 20),
-                    timing="CUDA-graph replay of K steps, CUDA events on the launch stream"),
+                    timing="CUDA-graph replay of K steps, CUDA events on the launch stream" +
+                           ("; max over ranks" if world > 1 else "")),
         tflops=round(nflops / per_step / 1e12, 2),
         roofline=dict(bound="hbm", achieved=round(value, 1), peak=peaks["hbm"], unit="GB/s",
                       frac=round(value / peaks["hbm"], 4), traffic=traffic,
                       peak_source=f"MEASURED_PEAKS.json hbm_gbs ({peaks['src']}); achieved = algorithmic bytes per "
                                   f"launch / average launch duration over the timed region (launches back to back)"),
-        e2e=dict(value=round(e2e_value, 1), unit="GB/s", h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h)),
-        gpu_launches=int((n_launch if world > 1 else gemm_launches) * args.steps),
+        e2e=dict(value=round(e2e_value, 1), unit="GB/s", h2d_bytes_per_step=int(h2d), d2h_bytes_per_step=int(d2h),
+                 copies_per_step="1 H2D (all activations) + 1 D2H (all outputs), pinned host memory, two copy "
+                                 "streams, double-buffered against the compute graph"),
+        gpu_launches=int(n_launch * args.steps),
         detail=detail,
     )
-    clk = clk.summary()
-    res["clocks"] = clk
+    if tp_detail:
+        res["tp"] = tp_detail
+    res["clocks"] = clk.summary()
     if world == 1 and not args.no_prefill:
-        tp, fl = prefill_leg(stream)
-        achieved = fl / tp / 1e12
+        tp_, fl, nsteps, pclk, td = prefill_leg(stream)
+        achieved = fl / tp_ / 1e12
         res["prefill"] = dict(
             workload="Llama-3-8B prefill GEMMs (qkv/o/gate_up/down) at M=8192, group 128, bf16 (BASELINE configs[2])",
-            us_per_step=round(tp * 1e6, 1), tflops=round(achieved, 1),
+            us_per_step=round(tp_ * 1e6, 1), tflops=round(achieved, 1), timed_steps=nsteps,
+            timed_seconds=round(tp_ * nsteps, 3), clocks=pclk,
+            dense_bf16_torch_matmul=dict(us_per_step=round(td * 1e6, 1), tflops=round(fl / td / 1e12, 1)),
             roofline=dict(bound="tensor", achieved=round(achieved, 1), peak=peaks["tc"], unit="TFLOP/s",
                           frac=round(achieved / peaks["tc"], 4),
                           peak_source=f"MEASURED_PEAKS.json bf16_tflops ({peaks['src']}, burst: cuBLAS bf16 8192^3)"))
@@ -423,6 +480,22 @@ def bench_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def self_launch(args):
+    """`bench.py --gpus N` run directly (no torchrun): start N ranks with torch.distributed.run
+    on this node (127.0.0.1 rendezvous); rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")              # communicator init (NVLink / NVLS) on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 # ---------------------------------------------------------------------------------- reference arm
@@ -484,7 +557,13 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         bench_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     else:
+        if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         bench_ours(args)
 
 

@@ -7,8 +7,19 @@
  * Conventions for every entry point
  *   - All tensor pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors)
  *     owned by the caller; the library keeps no reference after the call returns.
- *     The only device memory the library allocates is the per-stream stream-K
- *     workspace of tm_gemm_* (see below).
+ *     tm_gemm_w4a16_ws takes a caller-owned workspace and allocates nothing.  The
+ *     convenience entry points tm_gemm_w4a16 / _f16 / _partial_f32 instead use a
+ *     library-owned workspace, one per (device, stream), allocated with cudaMalloc on
+ *     the first call that needs it (a decode shape routed to the stream-K kernel) and
+ *     kept for the process lifetime; that first call must not be made inside CUDA-graph
+ *     capture (it returns TM_ERR_CUDA there).  All other state (TMA descriptors, kernel
+ *     attributes, SM counts, occupancy) is host-side and cached per device.
+ *   - Weights are read early: packed, scales and zeros may be read before the previous
+ *     kernel on `stream` has completed (programmatic dependent launch: the GEMM streams
+ *     its first weight chunks while the preceding kernel drains).  They must therefore not
+ *     be written by the kernel that immediately precedes the GEMM on its stream; tm_pack_w4
+ *     ends with a no-op kernel, so pack -> GEMM on one stream is safe.  Activations are
+ *     read only after the previous kernel has completed.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *     Every call only enqueues work on `stream` and returns; the caller keeps the
  *     buffers alive until the stream has completed.
@@ -46,6 +57,11 @@ typedef enum {
  * P:317-326) for the sm_100a data path.                                            */
 #define TM_LAYOUT_V1 1u
 
+/* Element types of tm_gemm_w4a16_ws. */
+#define TM_DTYPE_BF16 0
+#define TM_DTYPE_FP16 1
+#define TM_DTYPE_F32 2
+
 /* Host-side descriptor of a packed weight.  `data` is caller-owned device memory of
  * tm_pack_w4_bytes(K, N, group) bytes; tm_pack_w4 fills K, N, group and layout.    */
 typedef struct {
@@ -74,21 +90,29 @@ tm_status tm_pack_w4(const uint8_t* q, const void* scales, const void* zeros,
 
 /* Online W4A16 GEMM (§3.1 steps i-iv P:179-182, §3.4, §4.3 P:420-426;
  * §8(a) rows a3-a10):
- *     C[m][n] = RNE_bf16( sum_k A[m][k] * deq(q[k][n]) )   fp32 accumulation,
- * deq per reading R6 (weights rounded once to bf16 before the tensor-core MMA).
+ *     C[m][n] = RNE_bf16( sum_k A[m][k] * (q[k][n] - z[k/g][n]) * s[k/g][n] )
+ * with fp32 accumulation (the result is tolerance-checked, not bit-exact; R7, R12).
  *   A      : bf16 [M][K]                                                           (in)
  *   packed : descriptor filled by tm_pack_w4 (packed->K == K, packed->N == N)       (in)
  *   scales, zeros : fp16 [K/group][N] (group from the descriptor)                  (in)
  *   C      : bf16 [M][N]                                                           (out)
- * M <= 64 uses a persistent stream-K kernel (one CTA per SM, equal k-chunk ranges);
- * tiles shared by several CTAs are reduced in fixed k order through a library-owned
- * per-stream fp32 workspace (allocated on first use -- do that first call outside CUDA
- * graph capture).  Results are deterministic run to run.                              */
+ * Kernels (chosen on the host from M, N, K; tm_query_gemm_kind in tm_w4a16_debug.h):
+ *   M <= 64 : decode kernel (TMEM operand), reading R6b: the tensor-core operand is the
+ *             exact integer (q - z) in bf16 and the group scale s is applied in fp32 to the
+ *             per-group MMA result (C = sum_g s_g * sum_{k in g} (q - z) A); no weight
+ *             rounding.  K is split over a thread-block cluster reduced in distributed shared
+ *             memory when the tiles are few, else over a persistent stream-K grid whose
+ *             shared tiles are reduced through the workspace (fixed order: deterministic).
+ *   M > 64  : tiled (prefill) kernel, reading R6: weights rounded once to bf16,
+ *             RNE_bf16((q - z) * RNE_bf16(s)), before the MMA; for 65 <= M <= 512 K may be
+ *             split over a cluster (DSMEM reduction).
+ * Results are deterministic run to run.  Uses the library-owned workspace (see above).    */
 tm_status tm_gemm_w4a16(const void* A, const tm_packed_w4* packed,
                         const void* scales, const void* zeros, void* C,
                         int M, int N, int K, void* stream);
 
-/* Same with fp16 activations and fp16 output; deq = RNE_fp16((q - z) * s). */
+/* Same with fp16 activations and fp16 output (decode: exact (q - z) operand in fp16;
+ * prefill: deq = RNE_fp16((q - z) * s)).  Library-owned workspace.              */
 tm_status tm_gemm_w4a16_f16(const void* A, const tm_packed_w4* packed,
                             const void* scales, const void* zeros, void* C,
                             int M, int N, int K, void* stream);
@@ -99,6 +123,23 @@ tm_status tm_gemm_w4a16_f16(const void* A, const tm_packed_w4* packed,
 tm_status tm_gemm_w4a16_partial_f32(const void* A, const tm_packed_w4* packed,
                                     const void* scales, const void* zeros, float* C_partial,
                                     int M, int N, int K, void* stream);
+
+/* Workspace for tm_gemm_w4a16_ws: bytes needed for this shape (0 when the chosen kernel needs
+ * none), or a negative tm_status for an unsupported shape.                             */
+int64_t tm_gemm_workspace_bytes(int M, int N, int K, int group);
+
+/* The same GEMM with explicit element types and a caller-owned workspace (allocates nothing).
+ *   a_dtype   : TM_DTYPE_BF16 or TM_DTYPE_FP16 (A)
+ *   c_dtype   : a_dtype (rounded output) or TM_DTYPE_F32 (fp32 partial, bf16 A only)
+ *   workspace : device buffer of >= tm_gemm_workspace_bytes(M, N, K, group) bytes, 16-byte
+ *               aligned, ZERO-FILLED once before its first use (every call leaves it zeroed);
+ *               may be NULL (with workspace_bytes 0) when that size is 0.  One workspace
+ *               must not be used by two calls that can run concurrently.
+ * Errors: TM_ERR_INVALID_ARG for a missing/too small workspace or a dtype pair not listed. */
+tm_status tm_gemm_w4a16_ws(const void* A, const tm_packed_w4* packed,
+                           const void* scales, const void* zeros, void* C,
+                           int M, int N, int K, int a_dtype, int c_dtype,
+                           void* workspace, int64_t workspace_bytes, void* stream);
 
 /* out_bf16[i] = RNE_bf16(in_f32[i]) for i < count (TP epilogue after the all-reduce). */
 tm_status tm_tp_finalize(const float* in_f32, void* out_bf16, int64_t count, void* stream);
@@ -111,33 +152,6 @@ tm_status tm_tp_finalize(const float* in_f32, void* out_bf16, int64_t count, voi
 tm_status tm_unpack_w4(const tm_packed_w4* packed, uint8_t* q_out, void* stream);
 tm_status tm_dequant_w4(const tm_packed_w4* packed, const void* scales, const void* zeros,
                         void* W_out, int dtype, void* stream);
-
-/* Force a launch configuration (tests / benchmarking only).  tile_m in {16,32,64,128,256}
- * (<= 0: automatic).  split_k > 0: tiled kernel with split_k CTAs per tile along K (cluster
- * DSMEM reduction); split_k < 0: persistent stream-K kernel with -split_k CTAs; 0: automatic
- * (stream-K with one CTA per SM for tile_m <= 64, tiled kernel otherwise).
- * tm_query_gemm_config reports split_k < 0 for the stream-K kernel (its CTA count).      */
-tm_status tm_set_gemm_override(int tile_m, int split_k);
-
-/* Launch configuration the next tm_gemm_* call with these sizes would use. */
-tm_status tm_query_gemm_config(int M, int N, int K, int* tile_m, int* split_k, int* grid_ctas);
-
-/* Which kernel that configuration runs: 0 = tiled (prefill; split_k > 1 = CTAs per tile along
- * K in one cluster, chosen for 65 <= M <= 512 while tiles * split_k <= 128), 1 = persistent
- * stream-K decode, 2 = decode with split_k CTAs per tile reduced in distributed shared memory
- * over a thread-block cluster (chosen when few output tiles would leave SMs idle; split_k = 1:
- * one CTA per tile, no split, when 70-100 % of the SMs get a whole tile).              */
-tm_status tm_query_gemm_kind(int M, int N, int K, int* kind);
-
-/* Decode cluster mode (tests / benchmarking only): 0 automatic (default), 1 never (always
- * stream-K), 2..8 force that many CTAs per tile (capped by shared memory and K), -1 one CTA
- * per tile without a split.                                                            */
-tm_status tm_set_decode_cluster(int cs);
-
-/* Debug timeline: when buf != NULL every GEMM CTA writes 160 uint32 events (clock cycles
- * since CTA start; slot 0 = %globaltimer ns) at buf[cta * 160 + slot].  The buffer must
- * hold grid_ctas * 160 * 4 bytes.  NULL disables tracing (the default).               */
-tm_status tm_set_trace(void* buf, int64_t bytes);
 
 /* Human-readable status; library version string.                                     */
 const char* tm_status_string(tm_status status);

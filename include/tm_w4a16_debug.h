@@ -1,0 +1,50 @@
+/*
+ * tm_w4a16_debug.h -- test and measurement hooks of libtm_w4a16.so (not part of the product
+ * ABI in tm_w4a16.h).  The setters change process-global state read at launch time: call
+ * them only from single-threaded test or benchmark code, never while another thread issues
+ * GEMMs.  Everything here is exported by the same library.
+ */
+#ifndef TM_W4A16_DEBUG_H
+#define TM_W4A16_DEBUG_H
+
+#include "tm_w4a16.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Force a launch configuration.  tile_m in {16,32,64,128,256} (<= 0: automatic).  split_k > 0:
+ * tiled kernel with split_k CTAs per tile along K (cluster DSMEM reduction); split_k < 0 (tile_m
+ * <= 64): persistent stream-K decode kernel with -split_k CTAs; 0: automatic.                */
+tm_status tm_set_gemm_override(int tile_m, int split_k);
+
+/* Launch configuration the next tm_gemm_* call with these sizes would use (split_k < 0: the
+ * stream-K kernel's CTA count).                                                             */
+tm_status tm_query_gemm_config(int M, int N, int K, int* tile_m, int* split_k, int* grid_ctas);
+
+/* Which kernel that configuration runs: 0 = tiled (prefill; split_k > 1 = CTAs per tile along
+ * K in one cluster, chosen for 65 <= M <= 512 while tiles * split_k <= 128), 1 = persistent
+ * stream-K decode, 2 = decode with split_k CTAs per tile reduced in distributed shared memory
+ * over a thread-block cluster (split_k = 1: one CTA per tile).                               */
+tm_status tm_query_gemm_kind(int M, int N, int K, int* kind);
+
+/* Decode cluster mode: 0 automatic (default), 1 never (always stream-K), 2..8 force that many
+ * CTAs per tile (capped by shared memory and K), -1 one CTA per tile without a split.        */
+tm_status tm_set_decode_cluster(int cs);
+
+/* Debug timeline: when buf != NULL every GEMM CTA writes 160 uint32 events (clock cycles
+ * since CTA start; slot 0 = %globaltimer ns) at buf[cta * 160 + slot] (TM_PROFILE builds).
+ * NULL disables tracing (the default).                                                       */
+tm_status tm_set_trace(void* buf, int64_t bytes);
+
+/* The decode kernel's MMA operand for every weight (reading R6b), through the kernel's own
+ * dequantisation code: W_out[k][n] = (MAGIC + q) - (MAGIC + z) in bf16 (dtype 0) or fp16
+ * (dtype 1) -- exactly q - z for integer zeros.  zeros: fp16 [K/group][N].                  */
+tm_status tm_debug_dequant_int(const tm_packed_w4* packed, const void* zeros, void* W_out, int dtype,
+                               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TM_W4A16_DEBUG_H */

@@ -1,4 +1,5 @@
-"""ctypes binding of libtm_w4a16.so (include/tm_w4a16.h).  Argument marshalling only.
+"""ctypes binding of libtm_w4a16.so (include/tm_w4a16.h, include/tm_w4a16_debug.h).
+Argument marshalling only.
 
 Every function here forwards torch CUDA tensors as raw device pointers plus the
 current CUDA stream to the C ABI; all computation happens in the library's
@@ -16,6 +17,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TM_LIB_PATH") or os.path.join(_HERE, "libtm_w4a16.so")
 
 TM_LAYOUT_V1 = 1
+TM_DTYPE_BF16, TM_DTYPE_FP16, TM_DTYPE_F32 = 0, 1, 2
+_DT = {torch.bfloat16: TM_DTYPE_BF16, torch.float16: TM_DTYPE_FP16, torch.float32: TM_DTYPE_F32}
 
 _lib = None
 
@@ -43,6 +46,10 @@ _SIGS = {
     "tm_gemm_w4a16": (_I, [_P, ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _I, _I, _P]),
     "tm_gemm_w4a16_f16": (_I, [_P, ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _I, _I, _P]),
     "tm_gemm_w4a16_partial_f32": (_I, [_P, ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _I, _I, _P]),
+    "tm_gemm_workspace_bytes": (ctypes.c_int64, [_I, _I, _I, _I]),
+    "tm_gemm_w4a16_ws": (_I, [_P, ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _I, _I, _I, _I, _P,
+                              ctypes.c_int64, _P]),
+    "tm_debug_dequant_int": (_I, [ctypes.POINTER(tm_packed_w4), _P, _P, _I, _P]),
     "tm_tp_finalize": (_I, [_P, _P, ctypes.c_int64, _P]),
     "tm_unpack_w4": (_I, [ctypes.POINTER(tm_packed_w4), _P, _P]),
     "tm_dequant_w4": (_I, [ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _P]),
@@ -154,6 +161,35 @@ def gemm_w4a16_partial_f32(A, packed, scales, zeros, out=None, stream=None):
     return _gemm(lib().tm_gemm_w4a16_partial_f32, A, packed, scales, zeros, out, torch.float32, stream)
 
 
+def gemm_workspace_bytes(M, N, K, group):
+    """tm_gemm_workspace_bytes: bytes of caller workspace tm_gemm_w4a16_ws needs (0: none)."""
+    r = lib().tm_gemm_workspace_bytes(M, N, K, group)
+    if r < 0:
+        _check(int(r))
+    return int(r)
+
+
+def gemm_workspace(M, N, K, group, device="cuda"):
+    """A zero-filled workspace tensor for tm_gemm_w4a16_ws (None when the shape needs none)."""
+    n = gemm_workspace_bytes(M, N, K, group)
+    return torch.zeros(n, dtype=torch.uint8, device=device) if n else None
+
+
+def gemm_w4a16_ws(A, packed, scales, zeros, workspace, out=None, out_dtype=None, stream=None):
+    """tm_gemm_w4a16_ws: explicit dtypes (A bf16/fp16; C = A's dtype or fp32) and a caller-owned
+    workspace (torch uint8 CUDA tensor, zero-filled before first use, or None if not needed)."""
+    _require_cuda(A, scales, zeros)
+    M, K = A.shape
+    out_dtype = out_dtype or A.dtype
+    if out is None:
+        out = torch.empty((M, packed.N), dtype=out_dtype, device=A.device)
+    _require_cuda(out)
+    wp, wb = (None, 0) if workspace is None else (_ptr(workspace), workspace.numel())
+    _check(lib().tm_gemm_w4a16_ws(_ptr(A), ctypes.byref(packed.desc), _ptr(scales), _ptr(zeros), _ptr(out), M,
+                                  packed.N, K, _DT[A.dtype], _DT[out.dtype], wp, wb, _stream(stream)))
+    return out
+
+
 def tp_finalize(x_f32, out=None, stream=None):
     """tm_tp_finalize: fp32 -> bf16 (RNE)."""
     _require_cuda(x_f32)
@@ -175,6 +211,16 @@ def dequant_w4(packed, scales, zeros, dtype="bf16", stream=None):
     out = torch.empty((packed.K, packed.N), dtype=tdt, device=packed.data.device)
     _check(lib().tm_dequant_w4(ctypes.byref(packed.desc), _ptr(scales), _ptr(zeros), _ptr(out),
                                0 if dtype == "bf16" else 1, _stream(stream)))
+    return out
+
+
+def debug_dequant_int(packed, zeros, dtype="bf16", stream=None):
+    """tm_debug_dequant_int: the decode kernel's MMA operand (q - z) for every weight."""
+    _require_cuda(zeros)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float16
+    out = torch.empty((packed.K, packed.N), dtype=tdt, device=packed.data.device)
+    _check(lib().tm_debug_dequant_int(ctypes.byref(packed.desc), _ptr(zeros), _ptr(out),
+                                      0 if dtype == "bf16" else 1, _stream(stream)))
     return out
 
 

@@ -25,7 +25,7 @@ FLAGS = [
 
 def _inputs():
     files = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
-    files.append(os.path.join(ROOT, "include", "tm_w4a16.h"))
+    files += [os.path.join(ROOT, "include", h) for h in ("tm_w4a16.h", "tm_w4a16_debug.h")]
     return files
 
 

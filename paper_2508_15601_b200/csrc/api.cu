@@ -12,11 +12,10 @@
 #include <unordered_map>
 
 #include "../../include/tm_w4a16.h"
+#include "../../include/tm_w4a16_debug.h"
 #include "aux_kernels.cuh"
 #include "gemm_w4a16.cuh"
-#include "gemm_sk.cuh"
 #include "gemm_dec.cuh"
-#include "gemm_rf.cuh"
 
 namespace {
 
@@ -27,11 +26,7 @@ constexpr int kNumSMsDefault = 148;
 std::atomic<int> g_override_tile{0};
 std::atomic<int> g_override_split{0};
 std::atomic<int> g_dec_cluster{0};
-// register-fed decode kernel for M <= 16 (1 = on, 0 = TMEM decode kernel); TM_RF=0 for A/B runs
-std::atomic<int> g_rf{[] {
-  const char* e = std::getenv("TM_RF");
-  return e ? std::atoi(e) : 0;
-}()};  // 0 automatic, 1 never (stream-K), 2..8 forced size,
+ // 0 automatic, 1 never (stream-K), 2..8 forced size,
                                      // -1 one CTA per tile (no split)
 uint32_t* g_trace = nullptr;  // debug timeline buffer (tm_set_trace)
 
@@ -46,15 +41,43 @@ tm_status check_shape(int K, int N, int group) {
 
 tm_status from_cuda(cudaError_t e) { return e == cudaSuccess ? TM_OK : TM_ERR_CUDA; }
 
+// Everything cached about a device (SM count, configured kernel attributes, occupancy, the
+// library workspace) is kept per device ordinal: one process may drive several GPUs.
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  return dev;
+}
+
 int num_sms() {
-  static int sms = [] {
-    int dev = 0, v = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return kNumSMsDefault;
-    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
-      return kNumSMsDefault;
-    return v;
-  }();
-  return sms;
+  static std::atomic<int> sms[kMaxDevices] = {};
+  const int dev = current_device();
+  int v = sms[dev].load();
+  if (v > 0) return v;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+    (void)cudaGetLastError();
+    return kNumSMsDefault;  // no device (host-side configuration queries): B200
+  }
+  sms[dev].store(v);
+  return v;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
+template <typename Kern>
+tm_status ensure_smem(Kern kern, int bytes, std::atomic<int> (&done)[kMaxDevices]) {
+  const int dev = current_device();
+  if (done[dev].load() >= bytes) return TM_OK;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
+    (void)cudaGetLastError();  // do not leave a stale error for the next launch check
+    return TM_ERR_CUDA;
+  }
+  done[dev].store(bytes);
+  return TM_OK;
 }
 
 // ---------------------------------------------------------------- TMA descriptors
@@ -215,23 +238,32 @@ tm_status sz_tensor_map(const void* p, int G, int N, CUtensorMap* out, int rows 
 }
 
 // ---------------------------------------------------------------- stream-K workspace
-// Per-stream device buffer: [counters: 64K ints][fp32 partial slots].  Counters are zeroed once
-// at allocation and every kernel returns the ones it raised to zero before it exits (decode:
-// per-CTA partial flags, reset by the head holder; older stream-K: per-tile arrival counters,
-// reset by the last arriver).
+// The stream-K decode kernel needs [flags: one int per CTA, 256-B aligned][fp32 partial slots:
+// one NT x 128 tile per CTA].  Flags are zero between launches: the kernel returns every flag
+// it raised to zero before it exits.  Callers either pass their own buffer (tm_gemm_w4a16_ws;
+// zero-filled once before its first use) or use the library-owned one below.
+size_t ws_flag_bytes(int ctas) { return (static_cast<size_t>(ctas) * sizeof(int) + 255) & ~size_t(255); }
+
+// Library-owned workspace of the convenience entry points: one per (device, stream), allocated
+// on first use (outside CUDA-graph capture) and grown when a larger shape class needs more.
 struct Workspace {
   void* ptr = nullptr;
   size_t bytes = 0;
 };
-constexpr size_t kCounterBytes = 65536 * sizeof(int);
+struct WsKey {
+  int dev;
+  cudaStream_t stream;
+  bool operator==(const WsKey& o) const { return dev == o.dev && stream == o.stream; }
+};
+struct WsKeyHash {
+  size_t operator()(const WsKey& k) const { return reinterpret_cast<size_t>(k.stream) * 31u + k.dev; }
+};
 std::mutex g_ws_mu;
-std::unordered_map<cudaStream_t, Workspace> g_ws;
+std::unordered_map<WsKey, Workspace, WsKeyHash> g_ws;
 
-tm_status get_workspace(cudaStream_t stream, size_t partial_bytes, int n_counters, int** counters, float** partials) {
-  if (n_counters > 65536) return TM_ERR_UNSUPPORTED_SHAPE;
-  const size_t need = kCounterBytes + partial_bytes;
+tm_status library_workspace(cudaStream_t stream, size_t need, void** out) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  Workspace& w = g_ws[stream];
+  Workspace& w = g_ws[WsKey{current_device(), stream}];
   if (w.bytes < need) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
@@ -244,16 +276,33 @@ tm_status get_workspace(cudaStream_t stream, size_t partial_bytes, int n_counter
       w.ptr = nullptr;
       w.bytes = 0;
     }
-    size_t alloc = need < (size_t(16) << 20) ? (size_t(16) << 20) : need;
+    size_t alloc = need < (size_t(4) << 20) ? (size_t(4) << 20) : need;
     if (cudaMalloc(&w.ptr, alloc) != cudaSuccess) {
       (void)cudaGetLastError();
       return TM_ERR_CUDA;
     }
-    if (cudaMemset(w.ptr, 0, kCounterBytes) != cudaSuccess) return TM_ERR_CUDA;
+    if (cudaMemset(w.ptr, 0, alloc) != cudaSuccess) return TM_ERR_CUDA;
     w.bytes = alloc;
   }
-  *counters = static_cast<int*>(w.ptr);
-  *partials = reinterpret_cast<float*>(static_cast<uint8_t*>(w.ptr) + kCounterBytes);
+  *out = w.ptr;
+  return TM_OK;
+}
+
+// flags + partials for `ctas` CTAs of NT-token tiles, from the caller's buffer or the library's
+tm_status get_workspace(cudaStream_t stream, void* user, int64_t user_bytes, int ctas, int nt, int** flags,
+                        float** partials) {
+  const size_t fb = ws_flag_bytes(ctas);
+  const size_t need = fb + static_cast<size_t>(ctas) * nt * 128 * sizeof(float);
+  void* base = user;
+  if (user) {
+    if (user_bytes < static_cast<int64_t>(need)) return TM_ERR_INVALID_ARG;
+    if (!aligned16(user)) return TM_ERR_MISALIGNED;
+  } else {
+    tm_status st = library_workspace(stream, need, &base);
+    if (st != TM_OK) return st;
+  }
+  *flags = static_cast<int*>(base);
+  *partials = reinterpret_cast<float*>(static_cast<uint8_t*>(base) + fb);
   return TM_OK;
 }
 
@@ -281,8 +330,9 @@ int max_split_for(int nt) {
 // how many clusters of `cs` decode CTAs can be resident at once (one wave); cached per (nt, cs)
 template <int NT>
 int dec_active_clusters_t(int cs) {
-  static std::atomic<int> cache[9] = {};
-  int v = cache[cs].load();
+  static std::atomic<int> cache[kMaxDevices][9] = {};
+  const int dev = current_device();
+  int v = cache[dev][cs].load();
   if (v) return v;
   auto kern = w4a16_dec_kernel<NT, true, OUT_ACT>;
   const int fallback = num_sms() / cs;  // no device (host-side query): ideal packing
@@ -307,7 +357,7 @@ int dec_active_clusters_t(int cs) {
     n = fallback;
   }
   if (n < 1) n = 1;
-  cache[cs].store(n);
+  cache[dev][cs].store(n);
   return n;
 }
 int dec_active_clusters(int nt, int cs) {
@@ -357,18 +407,6 @@ Config choose_config(int M, int N, int K) {
     nt = 256;
   }
   const int n_tiles = N / 128;
-  if (ot <= 0 && g_override_split.load() == 0 && M <= 16 && g_rf.load()) {
-    // register-fed decode kernel (gemm_rf.cuh): persistent stream-K, one CTA per SM
-    c.kind = 3;
-    c.NT = M <= 8 ? 8 : 16;
-    const long long total = static_cast<long long>(n_tiles) * ((K + 255) / 256);
-    long long P = num_sms();
-    if (P > total) P = total;
-    c.split = static_cast<int>(P);
-    c.grid_x = c.split;
-    c.grid_y = 1;
-    return c;
-  }
   c.NT = nt;
   const int m_tiles = (M + nt - 1) / nt;
   const int KS = K / 64;
@@ -464,17 +502,10 @@ template <int NT, bool BF16, int OUT>
 tm_status launch_gemm_t(const CUtensorMap& map, const GemmArgs& args, const Config& c, cudaStream_t stream) {
   auto kern = w4a16_gemm_kernel<NT, BF16, OUT>;
   const int smem = GemmCfg<NT>::smem_bytes(c.split);
-  static int configured_smem = 0;  // per instantiation
+  static std::atomic<int> configured[kMaxDevices] = {};  // per instantiation and device
   if (c.split > GemmCfg<NT>::MAX_SPLIT) return TM_ERR_INVALID_ARG;
-  if (smem > configured_smem) {
-    const int max_smem = GemmCfg<NT>::smem_bytes(GemmCfg<NT>::MAX_SPLIT);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-    if (e != cudaSuccess) {
-      (void)cudaGetLastError();  // do not leave a stale error for the next launch check
-      return TM_ERR_CUDA;
-    }
-    configured_smem = max_smem;
-  }
+  tm_status sst = ensure_smem(kern, GemmCfg<NT>::smem_bytes(GemmCfg<NT>::MAX_SPLIT), configured);
+  if (sst != TM_OK) return sst;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(c.grid_x, c.grid_y, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -509,71 +540,19 @@ tm_status launch_gemm_t(const CUtensorMap& map, const GemmArgs& args, const Conf
   return TM_OK;
 }
 
-template <int NT, bool BF16, int OUT>
-tm_status launch_sk_t(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream) {
-  using Cfg = SkCfg<NT>;
-  auto kern = w4a16_sk_kernel<NT, BF16, OUT>;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess) {
-      (void)cudaGetLastError();
-      return TM_ERR_CUDA;
-    }
-    configured = true;
-  }
-  CUtensorMap ma, ms, mz;
-  tm_status st = act_tensor_map_3d(A, g.M, g.K, NT, Cfg::BLOBS, BF16, &ma);
-  if (st != TM_OK) return st;
-  st = sz_tensor_map(g.scales, g.K / g.group, g.N, &ms);
-  if (st != TM_OK) return st;
-  st = sz_tensor_map(g.zeros, g.K / g.group, g.N, &mz);
-  if (st != TM_OK) return st;
-  SkArgs a;
-  a.packed = g.packed;
-  a.out = g.out;
-  a.M = g.M;
-  a.N = g.N;
-  a.K = g.K;
-  a.group = g.group;
-  a.n_tiles = g.N / 128;
-  a.m_tiles = (g.M + NT - 1) / NT;
-  a.kc = (g.K + Cfg::CH - 1) / Cfg::CH;
-  a.total = static_cast<long long>(a.m_tiles) * a.n_tiles * a.kc;
-  a.trace = g_trace;
-  if (a.m_tiles * a.n_tiles > 65536) return TM_ERR_UNSUPPORTED_SHAPE;
-  st = get_workspace(stream, static_cast<size_t>(2) * c.split * NT * 128 * sizeof(float), a.m_tiles * a.n_tiles,
-                     &a.counters, &a.workspace);
-  if (st != TM_OK) return st;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(c.split, 1, 1);
-  cfg.blockDim = dim3(kSkThreads, 1, 1);
-  cfg.dynamicSmemBytes = Cfg::SMEM;
-  cfg.stream = stream;
-  cudaLaunchAttribute attrs[1];
-  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attrs[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attrs;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, ms, mz, a);
-  if (e != cudaSuccess) {
-    (void)cudaGetLastError();
-    return TM_ERR_CUDA;
-  }
-  return TM_OK;
-}
+// caller-owned workspace of tm_gemm_w4a16_ws (null: the library-owned one)
+struct UserWs {
+  void* ptr;
+  int64_t bytes;
+};
 
 template <int NT, bool BF16, int OUT, bool FS>
-tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream) {
+tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream, UserWs ws) {
   using Cfg = DecCfg<NT, FS>;
   auto kern = w4a16_dec_kernel<NT, BF16, OUT, FS>;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess) {
-      (void)cudaGetLastError();
-      return TM_ERR_CUDA;
-    }
-    configured = true;
-  }
+  static std::atomic<int> configured[kMaxDevices] = {};
+  tm_status sst = ensure_smem(kern, Cfg::SMEM, configured);
+  if (sst != TM_OK) return sst;
   CUtensorMap ma, ms, mz;
   tm_status st = act_tensor_map_3d(A, g.M, g.K, NT, Cfg::BLOBS, BF16, &ma);
   if (st != TM_OK) return st;
@@ -595,10 +574,14 @@ tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaSt
   a.trace = g_trace;
   a.cluster = c.kind == 2 ? c.split : 0;
   if (a.total * static_cast<long long>(c.split) >= (1ll << 32)) return TM_ERR_UNSUPPORTED_SHAPE;  // 32-bit range math
-  // one partial slot and one flag per CTA (its first segment)
-  st = get_workspace(stream, static_cast<size_t>(c.split) * NT * 128 * sizeof(float), c.split, &a.counters,
-                     &a.workspace);
-  if (st != TM_OK) return st;
+  // stream-K: one partial slot and one flag per CTA (its first segment); the cluster modes
+  // reduce in distributed shared memory and need no workspace
+  a.counters = nullptr;
+  a.workspace = nullptr;
+  if (c.kind == 1) {
+    st = get_workspace(stream, ws.ptr, ws.bytes, c.split, NT, &a.counters, &a.workspace);
+    if (st != TM_OK) return st;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(c.kind == 2 ? c.grid_x : c.split, 1, 1);
   cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
@@ -628,87 +611,20 @@ tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaSt
   return TM_OK;
 }
 
-template <int NT, int GROUP, bool BF16, int OUT>
-tm_status launch_rf_t(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream) {
-  using Cfg = RfCfg<NT, TM_RF_NG>;
-  auto kern = w4a16_rf_kernel<NT, TM_RF_NG, GROUP, BF16, OUT>;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess) {
-      (void)cudaGetLastError();
-      return TM_ERR_CUDA;
-    }
-    configured = true;
-  }
-  CUtensorMap ma, ms, mz;
-  tm_status st = act_tensor_map_3d(A, g.M, g.K, NT, 4, BF16, &ma);
-  if (st != TM_OK) return st;
-  st = sz_tensor_map(g.scales, g.K / g.group, g.N, &ms, 256 / GROUP);
-  if (st != TM_OK) return st;
-  st = sz_tensor_map(g.zeros, g.K / g.group, g.N, &mz, 256 / GROUP);
-  if (st != TM_OK) return st;
-  RfArgs a;
-  a.trace = g_trace;
-  a.packed = g.packed;
-  a.scales = g.scales;
-  a.zeros = g.zeros;
-  a.out = g.out;
-  a.M = g.M;
-  a.N = g.N;
-  a.K = g.K;
-  a.group = g.group;
-  a.n_tiles = g.N / 128;
-  a.kc = (g.K + Cfg::CH - 1) / Cfg::CH;
-  const long long total = static_cast<long long>(a.n_tiles) * a.kc;
-  if (total * c.split >= (1ll << 32)) return TM_ERR_UNSUPPORTED_SHAPE;  // 32-bit range math
-  a.total = static_cast<uint32_t>(total);
-  st = get_workspace(stream, static_cast<size_t>(c.split) * NT * 128 * sizeof(float), c.split, &a.flags,
-                     &a.workspace);
-  if (st != TM_OK) return st;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(c.split, 1, 1);
-  cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
-  cfg.dynamicSmemBytes = Cfg::SMEM;
-  cfg.stream = stream;
-  cudaLaunchAttribute attrs[1];
-  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attrs[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attrs;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, ms, mz, a);
-  if (e != cudaSuccess) {
-    (void)cudaGetLastError();
-    return TM_ERR_CUDA;
-  }
-  return TM_OK;
-}
-
-template <int NT, bool BF16, int OUT>
-tm_status launch_rf_g(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream) {
-  if (g.group == 64) return launch_rf_t<NT, 64, BF16, OUT>(A, g, c, stream);
-  return launch_rf_t<NT, 128, BF16, OUT>(A, g, c, stream);
-}
-
 template <bool BF16, int OUT>
-tm_status launch_sk(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream) {
-  if (c.kind == 3) {
-    if (c.NT == 8) return launch_rf_g<8, BF16, OUT>(A, g, c, stream);
-    return launch_rf_g<16, BF16, OUT>(A, g, c, stream);
-  }
+tm_status launch_sk(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream, UserWs ws) {
   switch (c.NT) {
     case 16: {
       // fused-scale variant (dequant sets apply the group scales; cluster split-K, group 128):
       // opt-in (TM_FS=1) -- measured 2.5 % slower on the bench mix in its final form
       static const bool fs = std::getenv("TM_FS") != nullptr;
-      if (fs && g.group == 128 && c.kind == 2) return launch_dec_t<16, BF16, OUT, true>(A, g, c, stream);
-      return launch_dec_t<16, BF16, OUT, false>(A, g, c, stream);
+      if (fs && g.group == 128 && c.kind == 2) return launch_dec_t<16, BF16, OUT, true>(A, g, c, stream, ws);
+      return launch_dec_t<16, BF16, OUT, false>(A, g, c, stream, ws);
     }
     // (NT = 32/64 keep the scale warps: measured with the fused variant, NT = 32 cluster shapes
     // were 6-13 % slower (2 dequant sets carry the scale work) and NT = 64 spills acc[64])
-    case 32: return launch_dec_t<32, BF16, OUT, false>(A, g, c, stream);
-    case 64: return launch_dec_t<64, BF16, OUT, false>(A, g, c, stream);
-    case 128: return launch_sk_t<128, BF16, OUT>(A, g, c, stream);
-    case 256: return launch_sk_t<256, BF16, OUT>(A, g, c, stream);
+    case 32: return launch_dec_t<32, BF16, OUT, false>(A, g, c, stream, ws);
+    case 64: return launch_dec_t<64, BF16, OUT, false>(A, g, c, stream, ws);
     default: return TM_ERR_INVALID_ARG;
   }
 }
@@ -726,7 +642,7 @@ tm_status launch_gemm(const CUtensorMap& map, const GemmArgs& args, const Config
 }
 
 tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* scales, const void* zeros, void* C,
-                      int M, int N, int K, void* stream, bool bf16, int out_kind) {
+                      int M, int N, int K, void* stream, bool bf16, int out_kind, UserWs ws = UserWs{nullptr, 0}) {
   if (!packed || !scales || !zeros || !packed->data) return TM_ERR_INVALID_ARG;
   if (M < 0) return TM_ERR_INVALID_ARG;
   if (packed->layout != TM_LAYOUT_V1 || packed->K != K || packed->N != N) return TM_ERR_INVALID_ARG;
@@ -748,11 +664,23 @@ tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* sca
   args.K = K;
   args.group = packed->group;
   args.split = c.split;
+  // raster band: keep band x NT x K x 2 B of activations (<= ~24 MB) L2-resident per band
+  {
+    const long long per = static_cast<long long>(c.NT) * K * 2;
+    long long b = per > 0 ? (24ll << 20) / per : 1;
+    if (b < 1) b = 1;
+    if (b > 16) b = 16;
+    static const int force_band = [] {  // A/B experiments only (1 = the old n-fastest order)
+      const char* e = std::getenv("TM_PREFILL_BAND");
+      return e ? std::atoi(e) : 0;
+    }();
+    args.band = force_band > 0 ? force_band : static_cast<int>(b);
+  }
   args.trace = g_trace;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (c.kind == 1 || c.kind == 2 || c.kind == 3) {
-    if (out_kind == OUT_F32) return launch_sk<true, OUT_F32>(A, args, c, s);
-    return bf16 ? launch_sk<true, OUT_ACT>(A, args, c, s) : launch_sk<false, OUT_ACT>(A, args, c, s);
+  if (c.kind == 1 || c.kind == 2) {
+    if (out_kind == OUT_F32) return launch_sk<true, OUT_F32>(A, args, c, s, ws);
+    return bf16 ? launch_sk<true, OUT_ACT>(A, args, c, s, ws) : launch_sk<false, OUT_ACT>(A, args, c, s, ws);
   }
   CUtensorMap map;
   st = act_tensor_map(A, M, K, c.NT, bf16, &map);
@@ -789,6 +717,9 @@ tm_status tm_pack_w4(const uint8_t* q, const void* scales, const void* zeros, in
   const long long chunks = static_cast<long long>(K) * N / 32;
   pack_w4_kernel<<<aux_grid(chunks, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       q, static_cast<uint4*>(packed->data), K, N);
+  // A GEMM reads its weights before griddepcontrol.wait (PDL); the no-op kernel makes sure the
+  // GEMM's predecessor is not the kernel that wrote them (it starts after the pack completed).
+  noop_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>();
   st = from_cuda(cudaGetLastError());
   if (st != TM_OK) return st;
   packed->K = K;
@@ -830,6 +761,24 @@ tm_status tm_dequant_w4(const tm_packed_w4* packed, const void* scales, const vo
   return from_cuda(cudaGetLastError());
 }
 
+tm_status tm_debug_dequant_int(const tm_packed_w4* packed, const void* zeros, void* W_out, int dtype, void* stream) {
+  if (!packed || !packed->data || !zeros || !W_out) return TM_ERR_INVALID_ARG;
+  if (packed->layout != TM_LAYOUT_V1 || (dtype != 0 && dtype != 1)) return TM_ERR_INVALID_ARG;
+  tm_status st = check_shape(packed->K, packed->N, packed->group);
+  if (st != TM_OK) return st;
+  if (!aligned16(packed->data) || !aligned16(zeros)) return TM_ERR_MISALIGNED;
+  const long long chunks = static_cast<long long>(packed->K) * packed->N / 32;
+  auto s = static_cast<cudaStream_t>(stream);
+  const auto in = static_cast<const uint4*>(packed->data);
+  const auto zr = static_cast<const uint16_t*>(zeros);
+  auto out = static_cast<uint16_t*>(W_out);
+  if (dtype == 0)
+    dequant_int_kernel<true><<<aux_grid(chunks, 256), 256, 0, s>>>(in, zr, out, packed->K, packed->N, packed->group);
+  else
+    dequant_int_kernel<false><<<aux_grid(chunks, 256), 256, 0, s>>>(in, zr, out, packed->K, packed->N, packed->group);
+  return from_cuda(cudaGetLastError());
+}
+
 tm_status tm_gemm_w4a16(const void* A, const tm_packed_w4* packed, const void* scales, const void* zeros, void* C,
                         int M, int N, int K, void* stream) {
   return gemm_common(A, packed, scales, zeros, C, M, N, K, stream, true, OUT_ACT);
@@ -843,6 +792,30 @@ tm_status tm_gemm_w4a16_f16(const void* A, const tm_packed_w4* packed, const voi
 tm_status tm_gemm_w4a16_partial_f32(const void* A, const tm_packed_w4* packed, const void* scales,
                                     const void* zeros, float* C_partial, int M, int N, int K, void* stream) {
   return gemm_common(A, packed, scales, zeros, C_partial, M, N, K, stream, true, OUT_F32);
+}
+
+int64_t tm_gemm_workspace_bytes(int M, int N, int K, int group) {
+  if (M < 0) return TM_ERR_INVALID_ARG;
+  const tm_status st = check_shape(K, N, group);
+  if (st != TM_OK) return st;
+  if (M == 0) return 0;
+  const Config c = choose_config(M, N, K);
+  if (c.kind != 1) return 0;
+  return static_cast<int64_t>(ws_flag_bytes(c.split) + static_cast<size_t>(c.split) * c.NT * 128 * sizeof(float));
+}
+
+tm_status tm_gemm_w4a16_ws(const void* A, const tm_packed_w4* packed, const void* scales, const void* zeros, void* C,
+                           int M, int N, int K, int a_dtype, int c_dtype, void* workspace, int64_t workspace_bytes,
+                           void* stream) {
+  if (a_dtype != TM_DTYPE_BF16 && a_dtype != TM_DTYPE_FP16) return TM_ERR_INVALID_ARG;
+  if (c_dtype != a_dtype && !(c_dtype == TM_DTYPE_F32 && a_dtype == TM_DTYPE_BF16)) return TM_ERR_INVALID_ARG;
+  if (workspace_bytes < 0 || (workspace == nullptr && workspace_bytes != 0)) return TM_ERR_INVALID_ARG;
+  if (M > 0 && workspace == nullptr) {
+    const int64_t need = tm_gemm_workspace_bytes(M, N, K, packed ? packed->group : 0);
+    if (need > 0) return TM_ERR_INVALID_ARG;  // this shape needs a workspace
+  }
+  return gemm_common(A, packed, scales, zeros, C, M, N, K, stream, a_dtype == TM_DTYPE_BF16,
+                     c_dtype == TM_DTYPE_F32 ? OUT_F32 : OUT_ACT, UserWs{workspace, workspace_bytes});
 }
 
 tm_status tm_tp_finalize(const float* in_f32, void* out_bf16, int64_t count, void* stream) {
@@ -865,6 +838,7 @@ tm_status tm_set_gemm_override(int tile_m, int split_k) {
     return TM_ERR_INVALID_ARG;
   if (split_k > 8 || (split_k > 0 && tile_m > 0 && split_k > max_split_for(tile_m))) return TM_ERR_INVALID_ARG;
   if (split_k < -4096) return TM_ERR_INVALID_ARG;
+  if (split_k < 0 && tile_m > 64) return TM_ERR_INVALID_ARG;  // stream-K is the decode kernel (tile_m <= 64)
   g_override_tile.store(tile_m > 0 ? tile_m : 0);
   g_override_split.store(split_k);
   return TM_OK;

@@ -103,6 +103,38 @@ __global__ void dequant_w4_kernel(const uint4* __restrict__ in, const uint16_t* 
   }
 }
 
+// The decode kernel's MMA operand (reading R6b): (MAGIC + q) - (MAGIC + z) per weight, through
+// its own deq_word_int / zero_operand code (debug entry tm_debug_dequant_int) -> W[K][N].
+template <bool BF16>
+__global__ void dequant_int_kernel(const uint4* __restrict__ in, const uint16_t* __restrict__ zeros,
+                                   uint16_t* __restrict__ W, int K, int N, int group) {
+  const int KS = K / 64;
+  const long long nchunks = static_cast<long long>(K) * N / 32;
+  for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < nchunks;
+       c += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const ChunkCoord cc = chunk_coord(c, KS);
+    const int n = cc.nt * 128 + cc.t;
+    const int kbase = cc.ks * 64 + cc.j * 32;
+    const int g = kbase / group;
+    const uint32_t z2 = zero_operand<BF16>(zeros[static_cast<size_t>(g) * N + n]);
+    const uint4 v = in[c];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int wj = 0; wj < 4; ++wj) {
+      uint32_t d[4];
+      deq_word_int<BF16>(w[wj], z2, d);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int k = kbase + wj * 8 + 2 * i;
+        W[static_cast<size_t>(k) * N + n] = static_cast<uint16_t>(d[i] & 0xFFFFu);
+        W[static_cast<size_t>(k + 1) * N + n] = static_cast<uint16_t>(d[i] >> 16);
+      }
+    }
+  }
+}
+
+__global__ void noop_kernel() {}
+
 // fp32 -> bf16 RNE (row-parallel TP epilogue after the fp32 all-reduce, reading R13).
 __global__ void tp_finalize_kernel(const float4* __restrict__ in, uint2* __restrict__ out, long long n4) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;

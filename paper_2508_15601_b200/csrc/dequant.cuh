@@ -98,15 +98,4 @@ __device__ __forceinline__ uint32_t zero_operand(uint16_t z_bits) {
   return static_cast<uint32_t>(zb) | (static_cast<uint32_t>(zb) << 16);
 }
 
-// MMA operand without the zero point: the 4 pairs (MAGIC + e_{2i}, MAGIC + e_{2i+1}) of one LAYOUT v1
-// word, exact (3 SHF + 4 LOP3).  Used by the register-fed decode kernel, which folds z and the
-// magic offset back in per group (gemm_rf.cuh).
-template <bool BF16>
-__device__ __forceinline__ void deq_word_magic(uint32_t w, uint32_t* out) {
-  constexpr uint32_t MAGIC = BF16 ? 0x43004300u : 0x64006400u;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(out[i]) : "r"(w >> (4 * i)), "r"(0x000F000Fu), "r"(MAGIC));
-}
-
 }  // namespace w4k

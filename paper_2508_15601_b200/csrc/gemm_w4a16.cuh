@@ -46,6 +46,7 @@ struct GemmArgs {
   void* out;               // [M][N] bf16/fp16 or fp32
   int M, N, K, group;
   int split;  // S: CTAs per tile along K (cluster size)
+  int band;   // m-tiles per raster band (tile order below); >= 1
   uint32_t* trace;  // optional per-CTA timeline (debug; nullptr in production)
 };
 
@@ -122,10 +123,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     args.trace[(blockIdx.y * gridDim.x + blockIdx.x) * kTraceSlots] = static_cast<uint32_t>(gt);
   }
 
+  // Tile order (L2 reuse): consecutive tiles walk a band of `band` m-tiles for one n-tile, then
+  // the next n-tile, so the CTAs resident at one time read each weight column from DRAM once per
+  // band (the band's activations, band x NT x K x 2 B, stay in L2); a CTA's split-K rank stays
+  // the fastest index so the S CTAs of a cluster take consecutive block ids.
   const int S = args.split;
-  const int nt = blockIdx.x / S;
   const int rank = blockIdx.x % S;
-  const int m0 = blockIdx.y * NT;
+  const int n_tiles = gridDim.x / S;
+  const int m_tiles = gridDim.y;
+  const int tile = (blockIdx.y * gridDim.x + blockIdx.x) / S;
+  const int band = args.band;
+  const int b0 = (tile / (band * n_tiles)) * band;           // first m-tile of this band
+  const int rows = min(band, m_tiles - b0);                   // m-tiles in this band
+  const int within = tile - b0 * n_tiles;
+  const int nt = within / rows;
+  const int m0 = (b0 + within % rows) * NT;
   const int KS = args.K / kBK;
   const int ks0 = static_cast<int>((static_cast<long long>(rank) * KS) / S);
   const int ks1 = static_cast<int>((static_cast<long long>(rank + 1) * KS) / S);

@@ -49,27 +49,42 @@ class ColumnParallelW4:
 
 
 class RowParallelW4:
-    """K-sharded W4A16 layer: fp32 partial + all-reduce + finalize."""
+    """K-sharded W4A16 layer: fp32 partial + all-reduce + finalize.  When K is not divisible into
+    `world` shards of whole groups (Qwen2-72B down: K = 29568 = 231 groups of 128), K is padded to
+    pad_k_to(K, world, group) with zero-weight groups (q = z = 0, s = 1; reading R9), so the
+    padded columns of the activations contribute exactly 0."""
 
     def __init__(self, q, s, z, group, world, rank, process_group=None):
         from . import api
         K, N = q.shape
-        self.lo, self.hi = shard_bounds(K, world, rank, group)
+        Kp = pad_k_to(K, world, group)
+        if Kp != K:
+            q = torch.cat([q, q.new_zeros(Kp - K, N)])
+            s = torch.cat([s, s.new_ones((Kp - K) // group, N)])
+            z = torch.cat([z, z.new_zeros((Kp - K) // group, N)])
+        self.lo, self.hi = shard_bounds(Kp, world, rank, group)
         g0, g1 = self.lo // group, self.hi // group
         self.s = s[g0:g1].contiguous()
         self.z = z[g0:g1].contiguous()
         self.packed = api.pack_w4(q[self.lo:self.hi].contiguous(), self.s, self.z, group)
-        self.K, self.N = K, N
+        self.K, self.Kp, self.N = K, Kp, N
         self.pg = process_group
 
     def local_partial(self, A_shard, out=None):
         from . import api
         return api.gemm_w4a16_partial_f32(A_shard, self.packed, self.s, self.z, out=out)
 
+    def shard_input(self, A):
+        """This rank's columns of the full activations A [M][K] (zero-padded past K)."""
+        if self.Kp != self.K:
+            A = torch.nn.functional.pad(A, (0, self.Kp - self.K))
+        return A[:, self.lo:self.hi].contiguous()
+
     def __call__(self, A, partial=None, out=None):
-        """A: full activations [M][K] (replicated); returns bf16 C [M][N] on every rank."""
+        """A: full activations [M][K] (replicated) or this rank's shard [M][hi - lo]; returns
+        bf16 C [M][N] on every rank."""
         from . import api
-        part = self.local_partial(A[:, self.lo:self.hi].contiguous() if A.shape[1] == self.K else A, out=partial)
+        part = self.local_partial(self.shard_input(A) if A.shape[1] == self.K else A, out=partial)
         if dist.is_initialized() and dist.get_world_size(self.pg) > 1:
             dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.pg)
         return api.tp_finalize(part, out=out)

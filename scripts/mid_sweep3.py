@@ -17,7 +17,7 @@ for name in ("qkv", "o", "gate_up", "down"):
         A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
         C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
         row = []
-        for tile, split in ((0, 0), (128, 1), (128, 2), (128, 3), (128, 4), (128, -148), (256, 1), (256, 2), (256, 4), (256, -148)):
+        for tile, split in ((0, 0), (128, 1), (128, 2), (128, 3), (128, 4), (256, 1), (256, 2), (256, 4),):
             if M <= 128 and tile == 256:
                 continue
             try:

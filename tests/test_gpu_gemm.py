@@ -14,6 +14,7 @@ from oracle.quant import dequant_rounded, dequant_f64
 from oracle.numerics import round_to
 from paper_2508_15601_b200 import api, synth
 from tests.gpu_helpers import to_dev, to_np64, bits16
+from tests.test_gpu_parity_r2 import _log
 
 pytestmark = pytest.mark.gpu
 
@@ -44,7 +45,8 @@ def _assert_parity(C, d, act="bf16", rows=None, tag=""):
     ref = gemm_f64(d["A"], d["q"], d["s"], d["z"], d["group"], rows=rows)
     got = to_np64(C) if rows is None else to_np64(C)[rows]
     r = compare.check(got, ref, d["A"], d["q"], d["s"], d["z"], d["group"], act)
-    assert r["ok"], (tag, r)
+    _log(tag, r)
+    assert r["ok"], (tag, compare.summary(r))
     return r
 
 
@@ -238,7 +240,7 @@ def test_m_zero_is_noop_and_errors():
         api.gemm_w4a16(t["A"], bad, t["s"], t["z"])
 
 
-SK_CASES = [(16, 1), (16, 3), (16, 7), (16, 148), (32, 5), (64, 4), (64, 148), (128, 3), (256, 2), (16, 2000)]
+SK_CASES = [(16, 1), (16, 3), (16, 7), (16, 148), (32, 5), (64, 4), (64, 148), (16, 2000)]
 
 
 @pytest.mark.parametrize("tile,P", SK_CASES)
