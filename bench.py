@@ -208,12 +208,14 @@ def step_bytes(ms, L):
 
 
 def time_graph(graph, steps, stream):
+    """Seconds for `steps` replays, CUDA events on `stream` (the replays are issued on it)."""
     import torch
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        graph.replay()
-    e1.record(stream)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(steps):
+            graph.replay()
+        e1.record(stream)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) * 1e-3
 
@@ -277,11 +279,11 @@ def prefill_leg(stream, min_seconds=1.0, M=8192):
     g = capture(lambda: [c() for c in calls], stream)
     gd = capture(lambda: [c() for c in dense], stream)
     t1 = time_graph(g, 2, stream) / 2
-    steps = max(5, int(min_seconds / t1) + 1)
+    steps = min(2000, max(5, int(min_seconds / t1) + 1))
     with ClockSampler(torch.cuda.current_device()) as clk:
         t = time_graph(g, steps, stream) / steps
-    td = time_graph(gd, max(5, int(min_seconds / 2 / t1) + 1), stream)
-    td /= max(5, int(min_seconds / 2 / t1) + 1)
+    nd = min(1000, max(5, int(min_seconds / 2 / t1) + 1))
+    td = time_graph(gd, nd, stream) / nd
     del keep, g, gd
     torch.cuda.empty_cache()
     return t, flops, steps, clk.summary(), td
@@ -362,7 +364,8 @@ def time_e2e(graphs, sets, host_A, host_C, steps, comp):
         comp.wait_event(ev_in[b])
         if i >= 2:
             comp.wait_event(ev_out[b])  # step i - 2's outputs have left this buffer
-        graphs[b].replay()
+        with torch.cuda.stream(comp):
+            graphs[b].replay()
         ev_comp[b].record(comp)
         d2h.wait_event(ev_comp[b])
         with torch.cuda.stream(d2h):
@@ -397,9 +400,7 @@ def bench_ours(args):
     # the whole step -- GEMMs and, under TP, the NCCL all-reduces -- is one CUDA graph
     graphs = [capture(lambda st=st: run_step(layers, st["io"], ms), stream) for st in sets]
     g = graphs[0]
-    for _ in range(2):
-        g.replay()
-    torch.cuda.synchronize()
+    time_graph(g, 2, stream)
     nbytes, nflops = step_bytes(ms, L)
     if world > 1:
         dist.barrier()

@@ -1,0 +1,50 @@
+"""Prefill (tiled kernel) timing per shape, CUDA-graph replay, with torch.matmul bf16 beside it.
+python scripts/prefill_perf.py [--ms 2048,4096,8192]"""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2508_15601_b200 import api, synth  # noqa: E402
+
+SHAPES = {"qkv": (6144, 4096), "o": (4096, 4096), "gate_up": (28672, 4096), "down": (4096, 14336)}
+
+
+def gtime(fn, reps=5):
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(reps):
+            g.replay()
+        e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e3
+
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--ms", default="2048,4096,8192")
+ap.add_argument("--shapes", default="qkv,o,gate_up,down")
+a = ap.parse_args()
+for name in a.shapes.split(","):
+    N, K = SHAPES[name]
+    d = synth.awq_like_torch(1, N, K, seed=3)
+    p = api.pack_w4(d["q"], d["s"], d["z"], 128)
+    W = torch.randn(K, N, device="cuda").to(torch.bfloat16)
+    for M in [int(x) for x in a.ms.split(",")]:
+        A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        t = gtime(lambda: api.gemm_w4a16(A, p, d["s"], d["z"], out=C))
+        td = gtime(lambda: torch.matmul(A, W, out=C))
+        fl = 2 * M * N * K
+        print(f"  {name:8s} M={M:5d}  w4a16 {t:8.1f} us {fl / t / 1e6:7.1f} TF/s   torch bf16 {td:8.1f} us "
+              f"{fl / td / 1e6:7.1f} TF/s   ratio {td / t:5.2f}", flush=True)
