@@ -289,6 +289,45 @@ def prefill_leg(stream, min_seconds=1.0, M=8192):
     return t, flops, steps, clk.summary(), td
 
 
+def moe_leg(stream, reps=20):
+    """Context leg (§8(f) NEXT-3, CFG#4 Mixtral expert shape N = 14336, K = 4096): decode of 8
+    experts with 4 routed tokens each (16 tokens, top-2) as ONE grouped launch vs one launch per
+    expert; 3 weight sets rotate (750 MB > L2).  GB/s = bytes of the experts read / time."""
+    import torch
+    from paper_2508_15601_b200 import api, synth
+    N, K, E, g, m = 14336, 4096, 8, 128, [4] * 8
+    sets = []
+    for rep in range(3):
+        ds = [synth.awq_like_torch(1, N, K, group=g, seed=900 + 10 * rep + e) for e in range(E)]
+        s_ = torch.stack([d["s"] for d in ds])
+        z_ = torch.stack([d["z"] for d in ds])
+        sets.append((api.pack_experts([d["q"] for d in ds], s_, z_, g), s_, z_,
+                     [api.pack_w4(d["q"], d["s"], d["z"], g) for d in ds], ds))
+    A = torch.randn(sum(m), K, device="cuda").to(torch.bfloat16)
+    C = torch.empty(sum(m), N, device="cuda", dtype=torch.bfloat16)
+    nbytes = E * (K * N // 2 + 4 * (K // g) * N) + 2 * sum(m) * (K + N)
+
+    def grouped(i):
+        pe, s_, z_, _, _ = sets[i % 3]
+        api.gemm_w4a16_grouped(A, pe, s_, z_, m, out=C)
+
+    def separate(i):
+        _, _, _, singles, ds = sets[i % 3]
+        for e in range(E):
+            api.gemm_w4a16(A[4 * e:4 * e + 4], singles[e], ds[e]["s"], ds[e]["z"], out=C[4 * e:4 * e + 4])
+
+    gg = capture(lambda: [grouped(i) for i in range(reps)], stream)
+    gs = capture(lambda: [separate(i) for i in range(reps)], stream)
+    tg = time_graph(gg, 3, stream) / 3 / reps
+    ts = time_graph(gs, 3, stream) / 3 / reps
+    del sets
+    torch.cuda.empty_cache()
+    return dict(workload="Mixtral-8x7B expert w1 (N=14336, K=4096, g=128), 8 experts x 4 tokens, bf16",
+                grouped_us=round(tg * 1e6, 2), grouped_GBps=round(nbytes / tg / 1e9, 1),
+                per_expert_launches_us=round(ts * 1e6, 2), per_expert_GBps=round(nbytes / ts / 1e9, 1),
+                grouped_frac_of_hbm=round(nbytes / tg / 1e9 / load_peaks()["hbm"], 4))
+
+
 def ncu_traffic(ms, L):
     """Per-launch DRAM traffic of the GEMM kernel from the committed ncu capture, if present."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -475,6 +514,8 @@ def bench_ours(args):
             roofline=dict(bound="tensor", achieved=round(achieved, 1), peak=peaks["tc"], unit="TFLOP/s",
                           frac=round(achieved / peaks["tc"], 4),
                           peak_source=f"MEASURED_PEAKS.json bf16_tflops ({peaks['src']}, burst: cuBLAS bf16 8192^3)"))
+    if world == 1 and not args.no_prefill:
+        res["moe"] = moe_leg(stream)
     if world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline()
     print(json.dumps(res), flush=True)

@@ -141,6 +141,26 @@ tm_status tm_gemm_w4a16_ws(const void* A, const tm_packed_w4* packed,
                            int M, int N, int K, int a_dtype, int c_dtype,
                            void* workspace, int64_t workspace_bytes, void* stream);
 
+/* Grouped W4A16 GEMM for mixture-of-experts layers (§8(f) NEXT-3; MoE models are evaluated
+ * in PAPER.md §5): n_experts independent problems of the same (N, K, group) in ONE
+ * launch,  C[r] = A[r] . W_e  for the rows r of expert e.
+ *   A            : bf16 [sum_e m_e][K], the tokens routed to expert 0 first, then expert 1, ...
+ *   packed       : the experts' LAYOUT v1 weights back to back (expert e at byte offset
+ *                  e * K * N / 2; pack each with tm_pack_w4 into its slice), descriptor
+ *                  K, N, group of ONE expert, bytes >= n_experts * K * N / 2
+ *   scales/zeros : fp16 [n_experts][K/group][N]
+ *   C            : bf16 [sum_e m_e][N], rows in the order of A
+ *   m_per_expert : HOST array [n_experts] of token counts m_e >= 0 (experts with m_e = 0 get
+ *                  no tiles: their weights are not read)
+ *   n_experts    : 1 .. 64
+ * The decode kernel (reading R6b) runs over the union of the experts' output tiles (cluster
+ * split-K or stream-K as for one GEMM, token tile = 16/32/64 from max m_e); deterministic.
+ * Library-owned workspace (see above).                                                      */
+tm_status tm_gemm_w4a16_grouped(const void* A, const tm_packed_w4* packed,
+                                const void* scales, const void* zeros, void* C,
+                                const int32_t* m_per_expert, int n_experts, int N, int K,
+                                void* stream);
+
 /* out_bf16[i] = RNE_bf16(in_f32[i]) for i < count (TP epilogue after the all-reduce). */
 tm_status tm_tp_finalize(const float* in_f32, void* out_bf16, int64_t count, void* stream);
 

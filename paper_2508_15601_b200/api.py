@@ -50,6 +50,8 @@ _SIGS = {
     "tm_gemm_w4a16_ws": (_I, [_P, ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _I, _I, _I, _I, _P,
                               ctypes.c_int64, _P]),
     "tm_debug_dequant_int": (_I, [ctypes.POINTER(tm_packed_w4), _P, _P, _I, _P]),
+    "tm_gemm_w4a16_grouped": (_I, [_P, ctypes.POINTER(tm_packed_w4), _P, _P, _P, ctypes.POINTER(ctypes.c_int32), _I,
+                                   _I, _I, _P]),
     "tm_tp_finalize": (_I, [_P, _P, ctypes.c_int64, _P]),
     "tm_unpack_w4": (_I, [ctypes.POINTER(tm_packed_w4), _P, _P]),
     "tm_dequant_w4": (_I, [ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _P]),
@@ -187,6 +189,39 @@ def gemm_w4a16_ws(A, packed, scales, zeros, workspace, out=None, out_dtype=None,
     wp, wb = (None, 0) if workspace is None else (_ptr(workspace), workspace.numel())
     _check(lib().tm_gemm_w4a16_ws(_ptr(A), ctypes.byref(packed.desc), _ptr(scales), _ptr(zeros), _ptr(out), M,
                                   packed.N, K, _DT[A.dtype], _DT[out.dtype], wp, wb, _stream(stream)))
+    return out
+
+
+class PackedExperts:
+    """E experts' LAYOUT v1 weights back to back in one device buffer + the grouped descriptor."""
+
+    def __init__(self, data, E, K, N, group):
+        self.data, self.E, self.K, self.N, self.group = data, E, K, N, group
+        self.desc = tm_packed_w4(data.data_ptr(), data.numel(), K, N, group, TM_LAYOUT_V1)
+
+
+def pack_experts(qs, scales, zeros, group, stream=None):
+    """Pack expert e's codes qs[e] (uint8 [K][N]) into slice e of one buffer with tm_pack_w4.
+    scales/zeros: fp16 [E][K/group][N] (contiguous)."""
+    E = len(qs)
+    K, N = qs[0].shape
+    per = pack_w4_bytes(K, N, group)
+    data = torch.empty(E * per, dtype=torch.uint8, device=qs[0].device)
+    for e in range(E):
+        pack_w4(qs[e], scales[e], zeros[e], group, stream=stream, out=data[e * per:(e + 1) * per])
+    return PackedExperts(data, E, K, N, group)
+
+
+def gemm_w4a16_grouped(A, packed_experts, scales, zeros, m_per_expert, out=None, stream=None):
+    """tm_gemm_w4a16_grouped: A bf16 [sum m_e][K] grouped by expert -> C bf16 [sum m_e][N]."""
+    _require_cuda(A, scales, zeros)
+    pe = packed_experts
+    counts = (ctypes.c_int32 * pe.E)(*[int(m) for m in m_per_expert])
+    if out is None:
+        out = torch.empty((A.shape[0], pe.N), dtype=torch.bfloat16, device=A.device)
+    _require_cuda(out)
+    _check(lib().tm_gemm_w4a16_grouped(_ptr(A), ctypes.byref(pe.desc), _ptr(scales), _ptr(zeros), _ptr(out), counts,
+                                       pe.E, pe.N, pe.K, _stream(stream)))
     return out
 
 

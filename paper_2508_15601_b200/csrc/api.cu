@@ -387,6 +387,56 @@ int dec_min_chunks() {
   return v;
 }
 
+// Decode kernel launch shape for `tiles` output tiles of NT tokens x 128 columns over K.
+// A few tiles (o/qkv/down-sized N) -> CS CTAs per tile in one cluster, reduced in distributed
+// shared memory (no global flags, no gpu-scope fences); else persistent stream-K.  Measured on
+// Llama-3-8B decode shapes: fixed per-CTA costs make ~8+ chunks of 256 k per CTA the sweet spot
+// -- o_proj 64 CTAs 6.6 us vs 128 CTAs 7.0 us vs stream-K 8.1 us -- and a cluster layout that
+// does not fit one wave is ~1.5x slower.
+Config decode_config(int nt, int tiles, int K) {
+  Config c{};
+  c.NT = nt;
+  const int kc = (K + 255) / 256;
+  const int force = g_dec_cluster.load();
+  const int cmax = dec_max_cluster(nt);
+  int cs = 0;
+  if (force >= 2) {
+    cs = force < cmax ? force : cmax;
+    if (cs > kc) cs = kc;
+  } else if (force == -1) {
+    cs = 1;
+  } else if (force == 0) {
+    for (int k = cmax; k >= 2; --k) {
+      if (k > kc || (kc + k - 1) / k < dec_min_chunks() || tiles * k > num_sms()) continue;
+      if (tiles > dec_active_clusters(nt, k)) continue;
+      cs = k;
+      break;
+    }
+  }
+  if (cs == 0 && force == 0 && tiles <= num_sms() && tiles * 10 >= 7 * num_sms()) {
+    // 70-100 % of the SMs have a whole tile each: one CTA per tile without a split beats
+    // stream-K's fix-ups (measured Mixtral expert N=14336 K=4096, 112 tiles, M=16:
+    // 12.5 -> 10.9 us at g=128; at 80 tiles -- Llama-3-70B qkv -- stream-K stays faster)
+    cs = 1;
+  }
+  if (cs >= 1) {
+    c.kind = 2;
+    c.split = cs;
+    c.grid_x = tiles * cs;
+    c.grid_y = 1;
+    return c;
+  }
+  // persistent stream-K: one CTA per SM, equal chunk ranges
+  c.kind = 1;
+  const long long total = static_cast<long long>(tiles) * kc;
+  long long P = num_sms();
+  if (P > total) P = total;
+  c.split = static_cast<int>(P);
+  c.grid_x = c.split;
+  c.grid_y = 1;
+  return c;
+}
+
 Config choose_config(int M, int N, int K) {
   Config c{};
   int nt = 16;
@@ -412,48 +462,7 @@ Config choose_config(int M, int N, int K) {
   const int KS = K / 64;
   int split = 1;
   const int os = g_override_split.load();
-  if (os == 0 && nt <= 64) {
-    // decode: a few tiles (o/qkv/down-sized N) -> CS CTAs per tile in one cluster, reduced in
-    // distributed shared memory (no global flags, no gpu-scope fences); else stream-K
-    // (measured on Llama-3-8B decode shapes: fixed per-CTA costs make ~8+ chunks of 256 k per
-    // CTA the sweet spot -- o_proj 64 CTAs 6.6 us vs 128 CTAs 7.0 us vs stream-K 8.1 us -- and a
-    // cluster layout that does not fit one wave is ~1.5x slower)
-    const int tiles = n_tiles * m_tiles;
-    const int kc = (K + 255) / 256;
-    const int force = g_dec_cluster.load();
-    const int cmax = dec_max_cluster(nt);
-    int cs = 0;
-    if (force >= 2) {
-      cs = force < cmax ? force : cmax;
-      if (cs > kc) cs = kc;
-    } else if (force == -1) {
-      c.kind = 2;
-      c.split = 1;
-      c.grid_x = tiles;
-      c.grid_y = 1;
-      return c;
-    } else if (force == 0) {
-      for (int k = cmax; k >= 2; --k) {
-        if (k > kc || (kc + k - 1) / k < dec_min_chunks() || tiles * k > num_sms()) continue;
-        if (tiles > dec_active_clusters(nt, k)) continue;
-        cs = k;
-        break;
-      }
-    }
-    if (cs == 0 && force == 0 && tiles <= num_sms() && tiles * 10 >= 7 * num_sms()) {
-      // 70-100 % of the SMs have a whole tile each: one CTA per tile without a split beats
-      // stream-K's fix-ups (measured Mixtral expert N=14336 K=4096, 112 tiles, M=16:
-      // 12.5 -> 10.9 us at g=128; at 80 tiles -- Llama-3-70B qkv -- stream-K stays faster)
-      cs = 1;
-    }
-    if (cs >= 1) {
-      c.kind = 2;
-      c.split = cs;
-      c.grid_x = tiles * cs;
-      c.grid_y = 1;
-      return c;
-    }
-  }
+  if (os == 0 && nt <= 64) return decode_config(nt, n_tiles * m_tiles, K);
   if (os < 0 || (os == 0 && nt <= 64)) {
     // persistent stream-K: one CTA per SM (or -os CTAs when forced), equal chunk ranges
     c.kind = 1;
@@ -546,20 +555,40 @@ struct UserWs {
   int64_t bytes;
 };
 
-template <int NT, bool BF16, int OUT, bool FS>
-tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream, UserWs ws) {
+// grouped (MoE) launch description: expert e's tiles, A/C rows and token count
+struct Grouped {
+  int E = 0;
+  int M_total = 0;
+  int tile_start[kMaxExperts + 1] = {};
+  int row_start[kMaxExperts] = {};
+  int m_count[kMaxExperts] = {};
+};
+
+template <int NT, bool BF16, int OUT, bool FS, typename GA = DecNoGroups>
+tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream, UserWs ws,
+                       const Grouped* grp = nullptr) {
   using Cfg = DecCfg<NT, FS>;
-  auto kern = w4a16_dec_kernel<NT, BF16, OUT, FS>;
+  auto kern = w4a16_dec_kernel<NT, BF16, OUT, FS, GA>;
   static std::atomic<int> configured[kMaxDevices] = {};
   tm_status sst = ensure_smem(kern, Cfg::SMEM, configured);
   if (sst != TM_OK) return sst;
   CUtensorMap ma, ms, mz;
+  const int E = grp ? grp->E : 1;
   tm_status st = act_tensor_map_3d(A, g.M, g.K, NT, Cfg::BLOBS, BF16, &ma);
   if (st != TM_OK) return st;
-  st = sz_tensor_map(g.scales, g.K / g.group, g.N, &ms);
+  st = sz_tensor_map(g.scales, E * (g.K / g.group), g.N, &ms);
   if (st != TM_OK) return st;
-  st = sz_tensor_map(g.zeros, g.K / g.group, g.N, &mz);
+  st = sz_tensor_map(g.zeros, E * (g.K / g.group), g.N, &mz);
   if (st != TM_OK) return st;
+  GA ga{};
+  if constexpr (std::is_same<GA, DecGroups>::value) {
+    ga.n_experts = grp->E;
+    for (int e = 0; e <= grp->E; ++e) ga.tile_start[e] = grp->tile_start[e];
+    for (int e = 0; e < grp->E; ++e) {
+      ga.row_start[e] = grp->row_start[e];
+      ga.m_count[e] = grp->m_count[e];
+    }
+  }
   DecArgs a;
   a.packed = g.packed;
   a.out = g.out;
@@ -570,7 +599,8 @@ tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaSt
   a.n_tiles = g.N / 128;
   a.m_tiles = (g.M + NT - 1) / NT;
   a.kc = (g.K + Cfg::CH - 1) / Cfg::CH;
-  a.total = static_cast<long long>(a.m_tiles) * a.n_tiles * a.kc;
+  a.total = grp ? static_cast<long long>(grp->tile_start[grp->E]) * a.kc
+               : static_cast<long long>(a.m_tiles) * a.n_tiles * a.kc;
   a.trace = g_trace;
   a.cluster = c.kind == 2 ? c.split : 0;
   if (a.total * static_cast<long long>(c.split) >= (1ll << 32)) return TM_ERR_UNSUPPORTED_SHAPE;  // 32-bit range math
@@ -603,7 +633,7 @@ tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaSt
     attrs[cfg.numAttrs].val.clusterDim.z = 1;
     ++cfg.numAttrs;
   }
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, ms, mz, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, ms, mz, a, ga);
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
     return TM_ERR_CUDA;
@@ -612,7 +642,18 @@ tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaSt
 }
 
 template <bool BF16, int OUT>
-tm_status launch_sk(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream, UserWs ws) {
+tm_status launch_sk(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream, UserWs ws,
+                    const Grouped* grp = nullptr) {
+  if (grp) {  // grouped (MoE) launches: bf16 in, bf16 out
+    if constexpr (BF16 && OUT == OUT_ACT) {
+      switch (c.NT) {
+        case 16: return launch_dec_t<16, true, OUT_ACT, false, DecGroups>(A, g, c, stream, ws, grp);
+        case 32: return launch_dec_t<32, true, OUT_ACT, false, DecGroups>(A, g, c, stream, ws, grp);
+        case 64: return launch_dec_t<64, true, OUT_ACT, false, DecGroups>(A, g, c, stream, ws, grp);
+      }
+    }
+    return TM_ERR_INVALID_ARG;
+  }
   switch (c.NT) {
     case 16: {
       // fused-scale variant (dequant sets apply the group scales; cluster split-K, group 128):
@@ -816,6 +857,48 @@ tm_status tm_gemm_w4a16_ws(const void* A, const tm_packed_w4* packed, const void
   }
   return gemm_common(A, packed, scales, zeros, C, M, N, K, stream, a_dtype == TM_DTYPE_BF16,
                      c_dtype == TM_DTYPE_F32 ? OUT_F32 : OUT_ACT, UserWs{workspace, workspace_bytes});
+}
+
+tm_status tm_gemm_w4a16_grouped(const void* A, const tm_packed_w4* packed, const void* scales, const void* zeros,
+                                void* C, const int32_t* m_per_expert, int n_experts, int N, int K, void* stream) {
+  if (!packed || !packed->data || !scales || !zeros || !m_per_expert) return TM_ERR_INVALID_ARG;
+  if (n_experts < 1 || n_experts > kMaxExperts) return TM_ERR_UNSUPPORTED_SHAPE;
+  if (packed->layout != TM_LAYOUT_V1 || packed->K != K || packed->N != N) return TM_ERR_INVALID_ARG;
+  tm_status st = check_shape(K, N, packed->group);
+  if (st != TM_OK) return st;
+  if (packed->bytes < static_cast<int64_t>(n_experts) * K * N / 2) return TM_ERR_INVALID_ARG;
+  Grouped grp;
+  grp.E = n_experts;
+  int max_m = 0;
+  for (int e = 0; e < n_experts; ++e) {
+    if (m_per_expert[e] < 0) return TM_ERR_INVALID_ARG;
+    grp.row_start[e] = grp.M_total;
+    grp.m_count[e] = m_per_expert[e];
+    grp.M_total += m_per_expert[e];
+    if (m_per_expert[e] > max_m) max_m = m_per_expert[e];
+  }
+  if (grp.M_total == 0) return TM_OK;  // no tokens routed: nothing to do
+  if (!A || !C) return TM_ERR_INVALID_ARG;
+  if (!aligned16(A) || !aligned16(packed->data) || !aligned16(scales) || !aligned16(zeros) || !aligned16(C))
+    return TM_ERR_MISALIGNED;
+  const int nt = max_m <= 16 ? 16 : (max_m <= 32 ? 32 : 64);
+  const int n_tiles = N / 128;
+  for (int e = 0; e < n_experts; ++e)  // experts with no tokens get no tiles (their weights stay unread)
+    grp.tile_start[e + 1] = grp.tile_start[e] + ((grp.m_count[e] + nt - 1) / nt) * n_tiles;
+  const Config c = decode_config(nt, grp.tile_start[n_experts], K);
+  GemmArgs args;
+  args.packed = static_cast<const uint8_t*>(packed->data);
+  args.scales = static_cast<const uint16_t*>(scales);
+  args.zeros = static_cast<const uint16_t*>(zeros);
+  args.out = C;
+  args.M = grp.M_total;
+  args.N = N;
+  args.K = K;
+  args.group = packed->group;
+  args.split = c.split;
+  args.band = 1;
+  args.trace = g_trace;
+  return launch_sk<true, OUT_ACT>(A, args, c, static_cast<cudaStream_t>(stream), UserWs{nullptr, 0}, &grp);
 }
 
 tm_status tm_tp_finalize(const float* in_f32, void* out_bf16, int64_t count, void* stream) {

@@ -81,6 +81,8 @@ namespace w4k {
 #endif
 
 
+constexpr int kMaxExperts = 64;
+
 struct DecArgs {
   const uint8_t* packed;  // LAYOUT v1
   void* out;              // [M][N] bf16/fp16 or fp32
@@ -94,6 +96,45 @@ struct DecArgs {
                           // (a thread-block cluster when CS > 1), tile = blockIdx.x / CS
   uint32_t* trace;
 };
+
+// Grouped launch (MoE, §8(f) NEXT-3; the kernel's GROUPED instantiation only, so the plain
+// launches keep a small parameter block): n_experts problems share one launch.  Expert e owns
+// tiles [tile_start[e], tile_start[e + 1]) (local tile index mt * n_tiles + nt), rows
+// [row_start[e], row_start[e] + m_count[e]) of A and C, packed weights at blob offset
+// e * n_tiles * (K / 64) and s/z group rows from e * K / group.
+struct DecGroups {
+  int n_experts;
+  int tile_start[kMaxExperts + 1];
+  int row_start[kMaxExperts];
+  int m_count[kMaxExperts];
+};
+struct DecNoGroups {};
+
+// Where tile t lives: its n-tile, first A/C row, valid rows (<= NT) and the expert's weight blob
+// and s/z group-row offsets.
+struct DecTile {
+  int nt, row0, mcount;
+  long long blob0;  // first 4 KB blob of the expert's packed weight
+  int g0;           // first s/z group row of the expert
+};
+template <int NT, typename GA>
+__device__ __forceinline__ DecTile dec_tile(const DecArgs& a, const GA& ga, int t) {
+  DecTile r;
+  int e = 0, local = t, rows = a.M, row_base = 0;
+  if constexpr (std::is_same<GA, DecGroups>::value) {
+    while (e + 1 < ga.n_experts && ga.tile_start[e + 1] <= t) ++e;
+    local = t - ga.tile_start[e];
+    rows = ga.m_count[e];
+    row_base = ga.row_start[e];
+  }
+  const int mt = static_cast<int>(static_cast<unsigned>(local) / static_cast<unsigned>(a.n_tiles));
+  r.nt = local - mt * a.n_tiles;
+  r.row0 = row_base + mt * NT;
+  r.mcount = rows - mt * NT < NT ? rows - mt * NT : NT;
+  r.blob0 = static_cast<long long>(e) * a.n_tiles * (a.K >> 6);
+  r.g0 = e * (a.K / a.group);
+  return r;
+}
 
 template <int NT, bool FS = false>
 struct DecCfg {
@@ -235,10 +276,10 @@ struct RingPos {
     if (const int t = static_cast<int>(u / kc); true)                                              \
       if ((cend = ((static_cast<uint32_t>(t) + 1) * kc < u1 ? (static_cast<uint32_t>(t) + 1) * kc : u1)), true)
 
-template <int NT, bool BF16, int OUT, bool FS = false>
+template <int NT, bool BF16, int OUT, bool FS = false, typename GA = DecNoGroups>
 __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
     w4a16_dec_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_s,
-                     const __grid_constant__ CUtensorMap tmap_z, const DecArgs args) {
+                     const __grid_constant__ CUtensorMap tmap_z, const DecArgs args, const __grid_constant__ GA groups) {
   using Cfg = DecCfg<NT, FS>;
   constexpr int NR = Cfg::NA;  // activation slots and per-chunk ready/done barriers
   constexpr int NW = Cfg::NW;
@@ -333,7 +374,8 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
   const auto produce_w = [&](int i_end) {  // weight chunks [w_i, i_end) of this CTA's range
     int i = 0;
     DEC_FOR_SEGMENTS {
-      const int nt = t % args.n_tiles;
+      const DecTile dt = dec_tile<NT>(args, groups, t);
+      const int nt = dt.nt;
       const int c0 = static_cast<int>(u - static_cast<uint32_t>(t) * kc);
       const int c1 = static_cast<int>(cend - static_cast<uint32_t>(t) * kc);
       for (int c = c0; c < c1; ++c, ++i) {
@@ -349,7 +391,8 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
           if (elect_one()) mbar_arrive(fb);
         } else if (elect_one()) {
           mbar_arrive_expect_tx(fb, nb * 4096);
-          bulk_g2s_hint(w0 + w_st.slot * Cfg::W_BYTES, args.packed + (static_cast<size_t>(nt) * KS + kb0) * 4096,
+          bulk_g2s_hint(w0 + w_st.slot * Cfg::W_BYTES,
+                        args.packed + (static_cast<size_t>(dt.blob0) + static_cast<size_t>(nt) * KS + kb0) * 4096,
                         nb * 4096, fb, w_policy);
         }
         __syncwarp();
@@ -415,8 +458,8 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
   // ---- segment end (scale warps, or dequant set 0 in FS mode: thread `row` = weight column, et =
   // its index among the 128 finishing threads).  acc = this CTA's sum over the segment's chunks.
   const auto seg_end = [&](float (&acc)[NT], int t, uint32_t u, uint32_t cend, int row, int et) {
-    const int nt = t % args.n_tiles;
-    const int mt = t / args.n_tiles;
+    const DecTile dt = dec_tile<NT>(args, groups, t);
+    const int nt = dt.nt;
     // ---- segment end.  A CTA's range [u0, u1) meets a shared tile only at its two ends: its
     // first segment may be the tile's tail (or a middle piece), its last segment the tile's
     // head.  The tail is computed first in time (start of the contributor's range), the head
@@ -427,8 +470,8 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
     const uint32_t tile_lo = static_cast<uint32_t>(t) * kc;
     const uint32_t tile_hi = tile_lo + kc;
     const int n = nt * 128 + row;
-    const int mb = mt * NT;
-    const int mcount = (args.M - mb) < NT ? (args.M - mb) : NT;
+    const int mb = dt.row0;
+    const int mcount = dt.mcount;
     if (push) {
       const uint32_t rank = cluster_ctarank();
       cluster_wait();  // pairs the setup arrive: the leader's bar_red is initialised
@@ -527,8 +570,8 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
     int i = 0, box = 0;
     bool waited_dep = false;
     DEC_FOR_SEGMENTS {
-      const int mt = t / args.n_tiles;
-      const int nt = t % args.n_tiles;
+      const DecTile dt = dec_tile<NT>(args, groups, t);
+      const int nt = dt.nt;
       const int c0 = static_cast<int>(u - static_cast<uint32_t>(t) * kc);
       const int c1 = static_cast<int>(cend - static_cast<uint32_t>(t) * kc);
       for (int c = c0; c < c1; ++c, ++i) {
@@ -536,7 +579,7 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
           const int j = box % Cfg::SZ_SLOTS;
           mbar_wait(bar_szempty + 8 * j, ((box / Cfg::SZ_SLOTS) & 1) ^ 1);
           const uint32_t fb = bar_szfull + 8 * j;
-          const int g0 = (c * Cfg::CH) >> gshift;
+          const int g0 = dt.g0 + ((c * Cfg::CH) >> gshift);
           if (elect_one()) {
             mbar_arrive_expect_tx(fb, 2 * Cfg::SZ_BOX);
             tma_load_2d(sz0 + j * 2 * Cfg::SZ_BOX, &tmap_s, nt * 128, g0, fb);
@@ -560,7 +603,7 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
           if (elect_one()) mbar_arrive(fb);
         } else if (elect_one()) {
           mbar_arrive_expect_tx(fb, Cfg::ACT_BYTES);
-          tma_load_3d(a0 + st.slot * Cfg::ACT_BYTES, &tmap_a, 0, mt * NT, c * Cfg::BLOBS, fb);
+          tma_load_3d(a0 + st.slot * Cfg::ACT_BYTES, &tmap_a, 0, dt.row0, c * Cfg::BLOBS, fb);
         }
         __syncwarp();
         st.advance(NR);
@@ -875,8 +918,6 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
     int ci = 0, box = -1;
     RingPos rps;
     DEC_FOR_SEGMENTS {
-      const int nt = t % args.n_tiles;
-      const int mt = t / args.n_tiles;
       const int c0 = static_cast<int>(u - static_cast<uint32_t>(t) * kc);
       const int c1 = static_cast<int>(cend - static_cast<uint32_t>(t) * kc);
       float acc[NT];
@@ -995,10 +1036,10 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
 #pragma unroll
         for (int m = 0; m < NT; ++m) acc_keep[m] += red[(q - 1) * NT * 128 + m * 128 + row];
       }
-      const int t = p / CS;
-      const int n = (t % args.n_tiles) * 128 + row;
-      const int mb = (t / args.n_tiles) * NT;
-      const int mcount = (args.M - mb) < NT ? (args.M - mb) : NT;
+      const DecTile dt = dec_tile<NT>(args, groups, p / CS);
+      const int n = dt.nt * 128 + row;
+      const int mb = dt.row0;
+      const int mcount = dt.mcount;
 #pragma unroll
       for (int m = 0; m < NT; ++m)
         if (m < mcount) dec_store<BF16, OUT>(args.out, args.N, mb + m, n, acc_keep[m]);
