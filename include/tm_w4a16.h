@@ -56,6 +56,9 @@ typedef enum {
  * inside each 32-bit word.  Realises PAPER.md §4.1 ("hardware-aware weight packing",
  * P:317-326) for the sm_100a data path.                                            */
 #define TM_LAYOUT_V1 1u
+/* W8 weights as LAYOUT v1 bit planes (tm_pack_w8): the [2K][N] nibble matrix of high planes
+ * (rows 0..K-1) then low planes (rows K..2K-1); only tm_gemm_w8a16 accepts it.             */
+#define TM_LAYOUT_V1_W8 2u
 
 /* Element types of tm_gemm_w4a16_ws. */
 #define TM_DTYPE_BF16 0
@@ -87,6 +90,37 @@ int64_t tm_pack_w4_bytes(int K, int N, int group);
  * (the GEMM consumes the raw [K/group][N] arrays).  Bit-exact to oracle/layout_v1.  */
 tm_status tm_pack_w4(const uint8_t* q, const void* scales, const void* zeros,
                      int K, int N, int group, tm_packed_w4* packed, void* stream);
+
+/* Checkpoint converters (§8(f) NEXT-4; AWQ/GPTQ checkpoints, §5):
+ * int4 checkpoints straight into LAYOUT v1 plus the fp16 zero points the GEMM takes; the
+ * checkpoint's fp16 scales [K/group][N] are used as they are.  Bit-exact to oracle/formats.py.
+ *   tm_pack_awq  : qweight int32 [K][N/8], qzeros int32 [K/group][N/8], nibble i of a word
+ *                  holds column 8j + (0,2,4,6,1,3,5,7)[i]
+ *   tm_pack_gptq : qweight int32 [K/8][N] (nibble i = row 8kb + i), qzeros int32 [K/group][N/8]
+ *                  (nibble i = column 8j + i, stored value = zero - zero_offset; zero_offset 1
+ *                  for GPTQ-v1 checkpoints, 0 for v2); no act-order (g_idx[k] = k / group)
+ *   packed    : as tm_pack_w4 (caller buffer of K*N/2 bytes; K, N, group, layout filled in)
+ *   zeros_out : fp16 [K/group][N] (device, caller-owned)                                   */
+tm_status tm_pack_awq(const int32_t* qweight, const int32_t* qzeros, int K, int N, int group,
+                      tm_packed_w4* packed, void* zeros_out, void* stream);
+tm_status tm_pack_gptq(const int32_t* qweight, const int32_t* qzeros, int K, int N, int group,
+                       int zero_offset, tm_packed_w4* packed, void* zeros_out, void* stream);
+
+/* 8-bit weights (W8A16; 4- and 8-bit weights, §2; §8(f) NEXT-4) by bit planes:
+ * with q8 = 16 hi + lo and z8 = 16 zh + zl, (q8 - z8) s = (hi - zh)(16 s) + (lo - zl) s exactly,
+ * so the W8 weight is packed as the W4 weight of 2K rows (high planes, then low planes) and
+ * multiplied by the activations twice along K (R17).
+ *   tm_pack_w8_bytes : K * N (K % 256 == 0 besides the W4 shape rules), or a negative status
+ *   tm_pack_w8  : q8 uint8 [K][N], scales fp16 [K/group][N], zeros8 fp16 [K/group][N] holding
+ *                 integers 0..255 -> packed (descriptor K = 2K, layout TM_LAYOUT_V1_W8),
+ *                 scales_out / zeros_out fp16 [2K/group][N] (caller buffers; 16 s must be finite)
+ *   tm_gemm_w8a16 : C bf16 [M][N] = A bf16 [M][K] . W8, with the tm_pack_w8 outputs; the
+ *                 decode/prefill kernels run over 2K and re-read A for the low planes.     */
+int64_t   tm_pack_w8_bytes(int K, int N, int group);
+tm_status tm_pack_w8(const uint8_t* q8, const void* scales, const void* zeros8, int K, int N, int group,
+                     tm_packed_w4* packed, void* scales_out, void* zeros_out, void* stream);
+tm_status tm_gemm_w8a16(const void* A, const tm_packed_w4* packed, const void* scales, const void* zeros,
+                        void* C, int M, int N, int K, void* stream);
 
 /* Online W4A16 GEMM (§3.1 steps i-iv P:179-182, §3.4, §4.3 P:420-426;
  * §8(a) rows a3-a10):

@@ -17,6 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TM_LIB_PATH") or os.path.join(_HERE, "libtm_w4a16.so")
 
 TM_LAYOUT_V1 = 1
+TM_LAYOUT_V1_W8 = 2
 TM_DTYPE_BF16, TM_DTYPE_FP16, TM_DTYPE_F32 = 0, 1, 2
 _DT = {torch.bfloat16: TM_DTYPE_BF16, torch.float16: TM_DTYPE_FP16, torch.float32: TM_DTYPE_F32}
 
@@ -50,6 +51,11 @@ _SIGS = {
     "tm_gemm_w4a16_ws": (_I, [_P, ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _I, _I, _I, _I, _P,
                               ctypes.c_int64, _P]),
     "tm_debug_dequant_int": (_I, [ctypes.POINTER(tm_packed_w4), _P, _P, _I, _P]),
+    "tm_pack_awq": (_I, [_P, _P, _I, _I, _I, ctypes.POINTER(tm_packed_w4), _P, _P]),
+    "tm_pack_gptq": (_I, [_P, _P, _I, _I, _I, _I, ctypes.POINTER(tm_packed_w4), _P, _P]),
+    "tm_pack_w8_bytes": (ctypes.c_int64, [_I, _I, _I]),
+    "tm_pack_w8": (_I, [_P, _P, _P, _I, _I, _I, ctypes.POINTER(tm_packed_w4), _P, _P, _P]),
+    "tm_gemm_w8a16": (_I, [_P, ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _I, _I, _P]),
     "tm_gemm_w4a16_grouped": (_I, [_P, ctypes.POINTER(tm_packed_w4), _P, _P, _P, ctypes.POINTER(ctypes.c_int32), _I,
                                    _I, _I, _P]),
     "tm_tp_finalize": (_I, [_P, _P, ctypes.c_int64, _P]),
@@ -189,6 +195,55 @@ def gemm_w4a16_ws(A, packed, scales, zeros, workspace, out=None, out_dtype=None,
     wp, wb = (None, 0) if workspace is None else (_ptr(workspace), workspace.numel())
     _check(lib().tm_gemm_w4a16_ws(_ptr(A), ctypes.byref(packed.desc), _ptr(scales), _ptr(zeros), _ptr(out), M,
                                   packed.N, K, _DT[A.dtype], _DT[out.dtype], wp, wb, _stream(stream)))
+    return out
+
+
+def pack_awq(qweight, qzeros, K, N, group, stream=None):
+    """tm_pack_awq: AWQ int4 checkpoint tensors -> (PackedW4, fp16 zeros [K/g][N])."""
+    _require_cuda(qweight, qzeros)
+    data = torch.empty(pack_w4_bytes(K, N, group), dtype=torch.uint8, device=qweight.device)
+    z = torch.empty((K // group, N), dtype=torch.float16, device=qweight.device)
+    p = PackedW4(data, K, N, group)
+    _check(lib().tm_pack_awq(_ptr(qweight), _ptr(qzeros), K, N, group, ctypes.byref(p.desc), _ptr(z), _stream(stream)))
+    return p, z
+
+
+def pack_gptq(qweight, qzeros, K, N, group, zero_offset=1, stream=None):
+    """tm_pack_gptq: GPTQ int4 checkpoint tensors -> (PackedW4, fp16 zeros [K/g][N])."""
+    _require_cuda(qweight, qzeros)
+    data = torch.empty(pack_w4_bytes(K, N, group), dtype=torch.uint8, device=qweight.device)
+    z = torch.empty((K // group, N), dtype=torch.float16, device=qweight.device)
+    p = PackedW4(data, K, N, group)
+    _check(lib().tm_pack_gptq(_ptr(qweight), _ptr(qzeros), K, N, group, zero_offset, ctypes.byref(p.desc), _ptr(z),
+                              _stream(stream)))
+    return p, z
+
+
+def pack_w8(q8, scales, zeros8, group, stream=None):
+    """tm_pack_w8: uint8 codes [K][N] + fp16 s, z8 [K/g][N] -> (packed bit planes, s4, z4 [2K/g][N])."""
+    _require_cuda(q8, scales, zeros8)
+    K, N = q8.shape
+    nb = lib().tm_pack_w8_bytes(K, N, group)
+    if nb < 0:
+        _check(int(nb))
+    data = torch.empty(int(nb), dtype=torch.uint8, device=q8.device)
+    s4 = torch.empty((2 * K // group, N), dtype=torch.float16, device=q8.device)
+    z4 = torch.empty((2 * K // group, N), dtype=torch.float16, device=q8.device)
+    p = PackedW4(data, 2 * K, N, group)
+    _check(lib().tm_pack_w8(_ptr(q8), _ptr(scales), _ptr(zeros8), K, N, group, ctypes.byref(p.desc), _ptr(s4), _ptr(z4),
+                            _stream(stream)))
+    return p, s4, z4
+
+
+def gemm_w8a16(A, packed8, s4, z4, out=None, stream=None):
+    """tm_gemm_w8a16: bf16 A [M][K] x W8 (tm_pack_w8 outputs) -> bf16 C [M][N]."""
+    _require_cuda(A, s4, z4)
+    M, K = A.shape
+    if out is None:
+        out = torch.empty((M, packed8.N), dtype=torch.bfloat16, device=A.device)
+    _require_cuda(out)
+    _check(lib().tm_gemm_w8a16(_ptr(A), ctypes.byref(packed8.desc), _ptr(s4), _ptr(z4), _ptr(out), M, packed8.N, K,
+                               _stream(stream)))
     return out
 
 

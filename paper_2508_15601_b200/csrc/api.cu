@@ -574,7 +574,7 @@ tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaSt
   if (sst != TM_OK) return sst;
   CUtensorMap ma, ms, mz;
   const int E = grp ? grp->E : 1;
-  tm_status st = act_tensor_map_3d(A, g.M, g.K, NT, Cfg::BLOBS, BF16, &ma);
+  tm_status st = act_tensor_map_3d(A, g.M, g.a_ks * 64, NT, Cfg::BLOBS, BF16, &ma);
   if (st != TM_OK) return st;
   st = sz_tensor_map(g.scales, E * (g.K / g.group), g.N, &ms);
   if (st != TM_OK) return st;
@@ -603,6 +603,7 @@ tm_status launch_dec_t(const void* A, const GemmArgs& g, const Config& c, cudaSt
                : static_cast<long long>(a.m_tiles) * a.n_tiles * a.kc;
   a.trace = g_trace;
   a.cluster = c.kind == 2 ? c.split : 0;
+  a.a_ks = g.a_ks;
   if (a.total * static_cast<long long>(c.split) >= (1ll << 32)) return TM_ERR_UNSUPPORTED_SHAPE;  // 32-bit range math
   // stream-K: one partial slot and one flag per CTA (its first segment); the cluster modes
   // reduce in distributed shared memory and need no workspace
@@ -682,11 +683,15 @@ tm_status launch_gemm(const CUtensorMap& map, const GemmArgs& args, const Config
   }
 }
 
+// a_K: columns of A (= K, or K / 2 for W8 bit planes: the low planes reuse the activations)
 tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* scales, const void* zeros, void* C,
-                      int M, int N, int K, void* stream, bool bf16, int out_kind, UserWs ws = UserWs{nullptr, 0}) {
+                      int M, int N, int K, void* stream, bool bf16, int out_kind, UserWs ws = UserWs{nullptr, 0},
+                      int a_K = 0) {
+  if (a_K == 0) a_K = K;
   if (!packed || !scales || !zeros || !packed->data) return TM_ERR_INVALID_ARG;
   if (M < 0) return TM_ERR_INVALID_ARG;
-  if (packed->layout != TM_LAYOUT_V1 || packed->K != K || packed->N != N) return TM_ERR_INVALID_ARG;
+  const uint32_t want_layout = a_K == K ? TM_LAYOUT_V1 : TM_LAYOUT_V1_W8;
+  if (packed->layout != want_layout || packed->K != K || packed->N != N) return TM_ERR_INVALID_ARG;
   tm_status st = check_shape(K, N, packed->group);
   if (st != TM_OK) return st;
   if (packed->bytes < static_cast<int64_t>(K) * N / 2) return TM_ERR_INVALID_ARG;
@@ -705,6 +710,7 @@ tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* sca
   args.K = K;
   args.group = packed->group;
   args.split = c.split;
+  args.a_ks = a_K / 64;
   // raster band: keep band x NT x K x 2 B of activations (<= ~24 MB) L2-resident per band
   {
     const long long per = static_cast<long long>(c.NT) * K * 2;
@@ -724,7 +730,7 @@ tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* sca
     return bf16 ? launch_sk<true, OUT_ACT>(A, args, c, s, ws) : launch_sk<false, OUT_ACT>(A, args, c, s, ws);
   }
   CUtensorMap map;
-  st = act_tensor_map(A, M, K, c.NT, bf16, &map);
+  st = act_tensor_map(A, M, a_K, c.NT, bf16, &map);
   if (st != TM_OK) return st;
   if (out_kind == OUT_F32) return launch_gemm<true, OUT_F32>(map, args, c, s);
   return bf16 ? launch_gemm<true, OUT_ACT>(map, args, c, s) : launch_gemm<false, OUT_ACT>(map, args, c, s);
@@ -768,6 +774,88 @@ tm_status tm_pack_w4(const uint8_t* q, const void* scales, const void* zeros, in
   packed->group = group;
   packed->layout = TM_LAYOUT_V1;
   return TM_OK;
+}
+
+namespace {
+tm_status finish_pack(tm_packed_w4* packed, int K, int N, int group, uint32_t layout, cudaStream_t s) {
+  noop_kernel<<<1, 32, 0, s>>>();  // the GEMM's predecessor is never the packing kernel (PDL)
+  const tm_status st = from_cuda(cudaGetLastError());
+  if (st != TM_OK) return st;
+  packed->K = K;
+  packed->N = N;
+  packed->group = group;
+  packed->layout = layout;
+  return TM_OK;
+}
+}  // namespace
+
+tm_status tm_pack_awq(const int32_t* qweight, const int32_t* qzeros, int K, int N, int group, tm_packed_w4* packed,
+                      void* zeros_out, void* stream) {
+  if (!qweight || !qzeros || !packed || !packed->data || !zeros_out) return TM_ERR_INVALID_ARG;
+  tm_status st = check_shape(K, N, group);
+  if (st != TM_OK) return st;
+  if (packed->bytes < static_cast<int64_t>(K) * N / 2) return TM_ERR_INVALID_ARG;
+  if (!aligned16(qweight) || !aligned16(qzeros) || !aligned16(packed->data) || !aligned16(zeros_out))
+    return TM_ERR_MISALIGNED;
+  auto s = static_cast<cudaStream_t>(stream);
+  const long long chunks = static_cast<long long>(K) * N / 32;
+  pack_awq_kernel<<<aux_grid(chunks, 256), 256, 0, s>>>(reinterpret_cast<const uint32_t*>(qweight),
+                                                        static_cast<uint4*>(packed->data), K, N);
+  const long long nz = static_cast<long long>(K / group) * N;
+  unpack_zeros_kernel<<<aux_grid(nz, 256), 256, 0, s>>>(reinterpret_cast<const uint32_t*>(qzeros),
+                                                        static_cast<uint16_t*>(zeros_out), nz, N, 1, 0);
+  return finish_pack(packed, K, N, group, TM_LAYOUT_V1, s);
+}
+
+tm_status tm_pack_gptq(const int32_t* qweight, const int32_t* qzeros, int K, int N, int group, int zero_offset,
+                       tm_packed_w4* packed, void* zeros_out, void* stream) {
+  if (!qweight || !qzeros || !packed || !packed->data || !zeros_out) return TM_ERR_INVALID_ARG;
+  if (zero_offset != 0 && zero_offset != 1) return TM_ERR_INVALID_ARG;
+  tm_status st = check_shape(K, N, group);
+  if (st != TM_OK) return st;
+  if (packed->bytes < static_cast<int64_t>(K) * N / 2) return TM_ERR_INVALID_ARG;
+  if (!aligned16(qweight) || !aligned16(qzeros) || !aligned16(packed->data) || !aligned16(zeros_out))
+    return TM_ERR_MISALIGNED;
+  auto s = static_cast<cudaStream_t>(stream);
+  const long long chunks = static_cast<long long>(K) * N / 32;
+  pack_gptq_kernel<<<aux_grid(chunks, 256), 256, 0, s>>>(reinterpret_cast<const uint32_t*>(qweight),
+                                                         static_cast<uint4*>(packed->data), K, N);
+  const long long nz = static_cast<long long>(K / group) * N;
+  unpack_zeros_kernel<<<aux_grid(nz, 256), 256, 0, s>>>(reinterpret_cast<const uint32_t*>(qzeros),
+                                                        static_cast<uint16_t*>(zeros_out), nz, N, 0, zero_offset);
+  return finish_pack(packed, K, N, group, TM_LAYOUT_V1, s);
+}
+
+int64_t tm_pack_w8_bytes(int K, int N, int group) {
+  const tm_status st = check_shape(K, N, group);
+  if (st != TM_OK) return st;
+  if (K % 256) return TM_ERR_UNSUPPORTED_SHAPE;  // a 256-k decode chunk never straddles the planes
+  return static_cast<int64_t>(K) * N;
+}
+
+tm_status tm_pack_w8(const uint8_t* q8, const void* scales, const void* zeros8, int K, int N, int group,
+                     tm_packed_w4* packed, void* scales_out, void* zeros_out, void* stream) {
+  if (!q8 || !scales || !zeros8 || !packed || !packed->data || !scales_out || !zeros_out) return TM_ERR_INVALID_ARG;
+  const int64_t need = tm_pack_w8_bytes(K, N, group);
+  if (need < 0) return static_cast<tm_status>(need);
+  if (packed->bytes < need) return TM_ERR_INVALID_ARG;
+  if (!aligned16(q8) || !aligned16(scales) || !aligned16(zeros8) || !aligned16(packed->data) ||
+      !aligned16(scales_out) || !aligned16(zeros_out))
+    return TM_ERR_MISALIGNED;
+  auto s = static_cast<cudaStream_t>(stream);
+  const long long chunks = static_cast<long long>(2 * K) * N / 32;
+  pack_w8_kernel<<<aux_grid(chunks, 256), 256, 0, s>>>(q8, static_cast<uint4*>(packed->data), K, N);
+  const long long nsz = static_cast<long long>(K / group) * N;
+  w8_sz_kernel<<<aux_grid(nsz, 256), 256, 0, s>>>(static_cast<const uint16_t*>(scales),
+                                                  static_cast<const uint16_t*>(zeros8), static_cast<uint16_t*>(scales_out),
+                                                  static_cast<uint16_t*>(zeros_out), nsz);
+  return finish_pack(packed, 2 * K, N, group, TM_LAYOUT_V1_W8, s);
+}
+
+tm_status tm_gemm_w8a16(const void* A, const tm_packed_w4* packed, const void* scales, const void* zeros, void* C,
+                        int M, int N, int K, void* stream) {
+  if (K <= 0 || K % 256) return K <= 0 ? TM_ERR_INVALID_ARG : TM_ERR_UNSUPPORTED_SHAPE;
+  return gemm_common(A, packed, scales, zeros, C, M, N, 2 * K, stream, true, OUT_ACT, UserWs{nullptr, 0}, K);
 }
 
 tm_status tm_unpack_w4(const tm_packed_w4* packed, uint8_t* q_out, void* stream) {
@@ -897,6 +985,7 @@ tm_status tm_gemm_w4a16_grouped(const void* A, const tm_packed_w4* packed, const
   args.group = packed->group;
   args.split = c.split;
   args.band = 1;
+  args.a_ks = K / 64;
   args.trace = g_trace;
   return launch_sk<true, OUT_ACT>(A, args, c, static_cast<cudaStream_t>(stream), UserWs{nullptr, 0}, &grp);
 }

@@ -135,6 +135,114 @@ __global__ void dequant_int_kernel(const uint4* __restrict__ in, const uint16_t*
 
 __global__ void noop_kernel() {}
 
+// ---------------------------------------------------------------- checkpoint converters (§8(f) NEXT-4)
+// LAYOUT v1 chunks straight from AWQ / GPTQ int4 checkpoints (formats: DESIGN.md §3, "checkpoint formats").
+// AWQ qweight int32 [K][N/8]: column n's code is nibble kAwqRev[n % 8] of word [k][n / 8].
+__device__ __forceinline__ int awq_rev(int c) { return (c & 1) * 4 + (c >> 1); }  // inverse of (0,2,4,6,1,3,5,7)
+
+__global__ void pack_awq_kernel(const uint32_t* __restrict__ qw, uint4* __restrict__ out, int K, int N) {
+  const int KS = K / 64;
+  const int NW = N / 8;
+  const long long nchunks = static_cast<long long>(K) * N / 32;
+  for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < nchunks;
+       c += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const ChunkCoord cc = chunk_coord(c, KS);
+    const int n = cc.nt * 128 + cc.t;
+    const int kbase = cc.ks * 64 + cc.j * 32;
+    const int sh = 4 * awq_rev(n & 7);
+    uint32_t w[4];
+#pragma unroll
+    for (int wj = 0; wj < 4; ++wj) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t code = (__ldg(qw + static_cast<size_t>(kbase + wj * 8 + e) * NW + (n >> 3)) >> sh) & 0xFu;
+        word |= code << (4 * nibble_of(e));
+      }
+      w[wj] = word;
+    }
+    out[c] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// GPTQ qweight int32 [K/8][N]: word [kb][n] holds rows 8 kb .. 8 kb + 7 of column n in nibbles
+// 0..7 -- exactly one LAYOUT v1 word, nibbles permuted to (e0 e2 e4 e6 e1 e3 e5 e7).
+__global__ void pack_gptq_kernel(const uint32_t* __restrict__ qw, uint4* __restrict__ out, int K, int N) {
+  const int KS = K / 64;
+  const long long nchunks = static_cast<long long>(K) * N / 32;
+  for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < nchunks;
+       c += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const ChunkCoord cc = chunk_coord(c, KS);
+    const int n = cc.nt * 128 + cc.t;
+    const int kbase = cc.ks * 64 + cc.j * 32;
+    uint32_t w[4];
+#pragma unroll
+    for (int wj = 0; wj < 4; ++wj) {
+      const uint32_t src = __ldg(qw + static_cast<size_t>((kbase + wj * 8) >> 3) * N + n);
+      uint32_t word = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) word |= ((src >> (4 * e)) & 0xFu) << (4 * nibble_of(e));
+      w[wj] = word;
+    }
+    out[c] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// zeros int32 [G][N/8] -> fp16 [G][N]: AWQ order (awq = 1) or sequential + offset (GPTQ)
+__global__ void unpack_zeros_kernel(const uint32_t* __restrict__ qz, uint16_t* __restrict__ z, long long count, int N,
+                                    int awq, int offset) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int n = static_cast<int>(i % N);
+    const long long g = i / N;
+    const int nib = awq ? awq_rev(n & 7) : (n & 7);
+    const int v = static_cast<int>((__ldg(qz + g * (N / 8) + (n >> 3)) >> (4 * nib)) & 0xFu) + offset;
+    z[i] = __half_as_ushort(__int2half_rn(v));
+  }
+}
+
+// W8 bit planes (reading R17): LAYOUT v1 of the [2K][N] nibble matrix whose row k < K is
+// q8[k] >> 4 and row K + k is q8[k] & 15.
+__global__ void pack_w8_kernel(const uint8_t* __restrict__ q8, uint4* __restrict__ out, int K, int N) {
+  const int K2 = 2 * K;
+  const int KS = K2 / 64;
+  const long long nchunks = static_cast<long long>(K2) * N / 32;
+  for (long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; c < nchunks;
+       c += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const ChunkCoord cc = chunk_coord(c, KS);
+    const int n = cc.nt * 128 + cc.t;
+    const int kbase = cc.ks * 64 + cc.j * 32;  // row of the [2K][N] plane matrix
+    const bool hi = kbase < K;
+    const int k8 = hi ? kbase : kbase - K;
+    uint32_t w[4];
+#pragma unroll
+    for (int wj = 0; wj < 4; ++wj) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t v = __ldg(q8 + static_cast<size_t>(k8 + wj * 8 + e) * N + n);
+        word |= (hi ? (v >> 4) : (v & 0xFu)) << (4 * nibble_of(e));
+      }
+      w[wj] = word;
+    }
+    out[c] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// W8 scales / zeros -> the planes' [2G][N]: high planes (16 s, z8 >> 4), low planes (s, z8 & 15)
+__global__ void w8_sz_kernel(const uint16_t* __restrict__ s, const uint16_t* __restrict__ z8, uint16_t* __restrict__ s4,
+                             uint16_t* __restrict__ z4, long long count) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const __half sv = __ushort_as_half(s[i]);
+    const int zv = __half2int_rn(__ushort_as_half(z8[i]));
+    s4[i] = __half_as_ushort(__hmul(sv, __float2half(16.0f)));  // exact (power of two) unless overflow
+    s4[count + i] = s[i];
+    z4[i] = __half_as_ushort(__int2half_rn((zv >> 4) & 0xF));
+    z4[count + i] = __half_as_ushort(__int2half_rn(zv & 0xF));
+  }
+}
+
 // fp32 -> bf16 RNE (row-parallel TP epilogue after the fp32 all-reduce, reading R13).
 __global__ void tp_finalize_kernel(const float4* __restrict__ in, uint2* __restrict__ out, long long n4) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;

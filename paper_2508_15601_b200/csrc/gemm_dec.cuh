@@ -94,6 +94,7 @@ struct DecArgs {
   long long total;        // m_tiles * n_tiles * kc
   int cluster;            // 0: persistent stream-K over [0, total); CS >= 1: CS CTAs per tile
                           // (a thread-block cluster when CS > 1), tile = blockIdx.x / CS
+  int a_ks;               // 64-k blobs of A along K: K / 64, or K / 128 for W8 bit planes (A reused)
   uint32_t* trace;
 };
 
@@ -603,7 +604,9 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
           if (elect_one()) mbar_arrive(fb);
         } else if (elect_one()) {
           mbar_arrive_expect_tx(fb, Cfg::ACT_BYTES);
-          tma_load_3d(a0 + st.slot * Cfg::ACT_BYTES, &tmap_a, 0, dt.row0, c * Cfg::BLOBS, fb);
+          // W8 bit planes: the low planes (k >= K_A) reuse the activations of the high planes
+          const int akb = c * Cfg::BLOBS >= args.a_ks ? c * Cfg::BLOBS - args.a_ks : c * Cfg::BLOBS;
+          tma_load_3d(a0 + st.slot * Cfg::ACT_BYTES, &tmap_a, 0, dt.row0, akb, fb);
         }
         __syncwarp();
         st.advance(NR);

@@ -47,6 +47,7 @@ struct GemmArgs {
   int M, N, K, group;
   int split;  // S: CTAs per tile along K (cluster size)
   int band;   // m-tiles per raster band (tile order below); >= 1
+  int a_ks;   // 64-k stages of A along K: K / 64, or K / 128 for W8 bit planes (A reused)
   uint32_t* trace;  // optional per-CTA timeline (debug; nullptr in production)
 };
 
@@ -224,7 +225,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(bar_empty + 8 * s, ph ^ 1);
         const uint32_t fb = bar_full + 8 * s;
         mbar_arrive_expect_tx(fb, Cfg::ACT_BYTES);
-        tma_load_2d(act0 + s * Cfg::ACT_BYTES, &tmap_a, (ks0 + i) * kBK, m0, fb);
+        const int aks = ks0 + i >= args.a_ks ? ks0 + i - args.a_ks : ks0 + i;  // W8: low planes reuse A
+        tma_load_2d(act0 + s * Cfg::ACT_BYTES, &tmap_a, aks * kBK, m0, fb);
       }
     }
     __syncwarp();
