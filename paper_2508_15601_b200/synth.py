@@ -92,3 +92,32 @@ def awq_like_torch(M, N, K, group=128, seed=1000, act_dtype="bf16", device="cuda
     A = torch.empty((M, K), device=device, dtype=torch.float32).normal_(0.0, 1.0, generator=gen).to(dt)
     return dict(A=A, q=q.reshape(K, N).contiguous(), s=s.contiguous(), z=z.to(torch.float16).contiguous(),
                 group=group, act_dtype=act_dtype)
+
+
+def quantize_kv(X, bits):
+    """KV-cache quantiser (SPEC.md S:110 min/max rule with group = the whole head_dim row, one
+    (scale, zero) per token and KV head; "per head, per token, groups along the channel
+    dimension").  X float [..., D] -> codes uint8 [..., D] (0 .. 2^bits - 1), scale fp16 [...],
+    zero fp16 [...] (integer-valued)."""
+    qmax = (1 << bits) - 1
+    mn = X.min(axis=-1)
+    mx = X.max(axis=-1)
+    s = np.maximum((mx - mn) / qmax, SCALE_EPS).astype(np.float16)
+    sf = s.astype(np.float32)
+    z = np.clip(np.rint(-mn / sf), 0, qmax)
+    q = np.clip(np.rint(X / sf[..., None]) + z[..., None], 0, qmax).astype(np.uint8)
+    return q, s, z.astype(np.float16)
+
+
+def kv_decode_problem(B, Hq, Hkv, D, Lmax, seq_lens, bits, seed=1000, act_dtype="bf16"):
+    """A decode-attention step: Q ~ N(0, 1) [B][Hq][D] rounded to the activation
+    dtype; K, V ~ N(0, 1) [B][Hkv][Lmax][D] quantised per (token, head) by quantize_kv.
+    Returns dict(Q, kq, ks, kz, vq, vs, vz, seq_lens) with codes uint8 [B][Hkv][Lmax][D]."""
+    rng = np.random.default_rng(seed)
+    Q = round_act(rng.normal(size=(B, Hq, D)).astype(np.float32), act_dtype)
+    Kf = rng.normal(size=(B, Hkv, Lmax, D)).astype(np.float32)
+    Vf = rng.normal(size=(B, Hkv, Lmax, D)).astype(np.float32)
+    kq, ks, kz = quantize_kv(Kf, bits)
+    vq, vs, vz = quantize_kv(Vf, bits)
+    return dict(Q=Q, kq=kq, ks=ks, kz=kz, vq=vq, vs=vs, vz=vz, seq_lens=np.asarray(seq_lens, dtype=np.int32),
+                bits=bits, act_dtype=act_dtype)
