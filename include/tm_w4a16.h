@@ -195,6 +195,24 @@ tm_status tm_gemm_w4a16_grouped(const void* A, const tm_packed_w4* packed,
                                 const int32_t* m_per_expert, int n_experts, int N, int K,
                                 void* stream);
 
+/* Low-bit-KV decode attention (§8(f) NEXT-2; the paper's attention pipeline, §3.4 P:276-280,
+ * §4.2, §4.4): one decode step, 8-bit KV cache, head_dim 128,
+ *     O[b][h] = sum_t softmax_t(scale Q[b][h] . K[t]) V[t],   t < seq_lens[b],
+ *     K[t] = (k_codes[t] - kz[t]) ks[t] (one fp16 (scale, zero) per token and KV head; V alike),
+ * KV head h / G serves query head h (grouped-query attention, G = Hq / Hkv in {1, 2, 4, 8}).
+ *   Q        : [B][Hq][128] bf16 (q_dtype TM_DTYPE_BF16) or fp16; O : same shape and dtype
+ *   k_codes, v_codes : uint8 [B][Hkv][Lmax][128], Lmax % 64 == 0 (cache capacity)
+ *   k_sz, v_sz : uint32 [B][Hkv][Lmax], fp16 scale in the low half, fp16 zero in the high half
+ *   seq_lens : int32 [B] on the device, 1 <= seq_lens[b] <= Lmax
+ *   workspace: tm_attn_workspace_bytes(B, Hq, Hkv, Lmax) bytes (0 when Lmax <= 256: NULL is
+ *              fine), zero-filled once before first use, left zeroed; not shared by concurrent calls
+ * Deterministic; fp32 softmax and accumulation, one rounding of O (R18).          */
+int64_t   tm_attn_workspace_bytes(int B, int Hq, int Hkv, int Lmax);
+tm_status tm_attn_decode_kv8(const void* Q, const void* k_codes, const void* v_codes, const void* k_sz,
+                             const void* v_sz, const int32_t* seq_lens, void* O, int B, int Hq, int Hkv,
+                             int Lmax, float softmax_scale, int q_dtype, void* workspace,
+                             int64_t workspace_bytes, void* stream);
+
 /* out_bf16[i] = RNE_bf16(in_f32[i]) for i < count (TP epilogue after the all-reduce). */
 tm_status tm_tp_finalize(const float* in_f32, void* out_bf16, int64_t count, void* stream);
 

@@ -56,6 +56,9 @@ _SIGS = {
     "tm_pack_w8_bytes": (ctypes.c_int64, [_I, _I, _I]),
     "tm_pack_w8": (_I, [_P, _P, _P, _I, _I, _I, ctypes.POINTER(tm_packed_w4), _P, _P, _P]),
     "tm_gemm_w8a16": (_I, [_P, ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _I, _I, _P]),
+    "tm_attn_workspace_bytes": (ctypes.c_int64, [_I, _I, _I, _I]),
+    "tm_attn_decode_kv8": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, ctypes.c_float, _I, _P, ctypes.c_int64,
+                                _P]),
     "tm_gemm_w4a16_grouped": (_I, [_P, ctypes.POINTER(tm_packed_w4), _P, _P, _P, ctypes.POINTER(ctypes.c_int32), _I,
                                    _I, _I, _P]),
     "tm_tp_finalize": (_I, [_P, _P, ctypes.c_int64, _P]),
@@ -245,6 +248,36 @@ def gemm_w8a16(A, packed8, s4, z4, out=None, stream=None):
     _check(lib().tm_gemm_w8a16(_ptr(A), ctypes.byref(packed8.desc), _ptr(s4), _ptr(z4), _ptr(out), M, packed8.N, K,
                                _stream(stream)))
     return out
+
+
+def attn_workspace(B, Hq, Hkv, Lmax, device="cuda"):
+    """Zero-filled workspace tensor for tm_attn_decode_kv8 (None when not needed)."""
+    n = lib().tm_attn_workspace_bytes(B, Hq, Hkv, Lmax)
+    if n < 0:
+        _check(int(n))
+    return torch.zeros(int(n), dtype=torch.uint8, device=device) if n else None
+
+
+def attn_decode_kv8(Q, k_codes, v_codes, k_sz, v_sz, seq_lens, workspace=None, scale=None, out=None, stream=None):
+    """tm_attn_decode_kv8: Q [B][Hq][128] bf16/fp16, codes uint8 [B][Hkv][Lmax][128], sz uint32
+    [B][Hkv][Lmax] (fp16 scale | zero << 16), seq_lens int32 [B] (device) -> O like Q."""
+    _require_cuda(Q, k_codes, v_codes, k_sz, v_sz, seq_lens)
+    B, Hq, D = Q.shape
+    _, Hkv, Lmax, _ = k_codes.shape
+    if out is None:
+        out = torch.empty_like(Q)
+    wp, wb = (None, 0) if workspace is None else (_ptr(workspace), workspace.numel())
+    sc = float(scale if scale is not None else 1.0 / D ** 0.5)
+    _check(lib().tm_attn_decode_kv8(_ptr(Q), _ptr(k_codes), _ptr(v_codes), _ptr(k_sz), _ptr(v_sz), _ptr(seq_lens),
+                                    _ptr(out), B, Hq, Hkv, Lmax, sc, _DT[Q.dtype], wp, wb, _stream(stream)))
+    return out
+
+
+def pack_kv_sz(scale, zero):
+    """fp16 scale and zero tensors [...] -> uint32 [...] (scale in the low half) for the KV cache."""
+    s = scale.contiguous().view(torch.int16).to(torch.int32) & 0xFFFF
+    z = zero.contiguous().view(torch.int16).to(torch.int32) & 0xFFFF
+    return (s | (z << 16)).contiguous()
 
 
 class PackedExperts:

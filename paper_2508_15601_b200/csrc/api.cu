@@ -16,6 +16,7 @@
 #include "aux_kernels.cuh"
 #include "gemm_w4a16.cuh"
 #include "gemm_dec.cuh"
+#include "attn_dec.cuh"
 
 namespace {
 
@@ -226,6 +227,37 @@ tm_status sz_tensor_map(const void* p, int G, int N, CUtensorMap* out, int rows 
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(p), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return TM_ERR_CUDA;
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    if (g_maps.size() > 4096) g_maps.clear();
+    g_maps.emplace(key, map);
+  }
+  *out = map;
+  return TM_OK;
+}
+
+// 2-D map over an 8-bit KV cache viewed as uint8 rows of 128 codes: box {128, 64 tokens}, SW128.
+tm_status kv_tensor_map(const void* p, long long rows, CUtensorMap* out) {
+  const MapKey key{p, static_cast<int>(rows & 0x7fffffff), static_cast<int>(rows >> 31), 64 | (3 << 28), 3};
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return TM_OK;
+    }
+  }
+  auto enc = get_encode();
+  if (!enc) return TM_ERR_CUDA;
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {128, static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {128, 64};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(p), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return TM_ERR_CUDA;
   {
@@ -746,6 +778,41 @@ int aux_grid(long long work, int block) {
 
 }  // namespace
 
+namespace {
+template <int G, bool BF16>
+tm_status launch_attn_t(const CUtensorMap& mk, const CUtensorMap& mv, const AttnArgs& a, cudaStream_t s) {
+  auto kern = attn_dec_kernel<G, BF16>;
+  static std::atomic<int> configured[kMaxDevices] = {};
+  tm_status st = ensure_smem(kern, AttnCfg<G>::SMEM, configured);
+  if (st != TM_OK) return st;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.splits, a.Hkv, a.B);
+  cfg.blockDim = dim3(128, 1, 1);
+  cfg.dynamicSmemBytes = AttnCfg<G>::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, mk, mv, a) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return TM_ERR_CUDA;
+  }
+  return TM_OK;
+}
+template <bool BF16>
+tm_status launch_attn(int G, const CUtensorMap& mk, const CUtensorMap& mv, const AttnArgs& a, cudaStream_t s) {
+  switch (G) {
+    case 1: return launch_attn_t<1, BF16>(mk, mv, a, s);
+    case 2: return launch_attn_t<2, BF16>(mk, mv, a, s);
+    case 4: return launch_attn_t<4, BF16>(mk, mv, a, s);
+    case 8: return launch_attn_t<8, BF16>(mk, mv, a, s);
+  }
+  return TM_ERR_UNSUPPORTED_SHAPE;
+}
+}  // namespace
+
 extern "C" {
 
 int64_t tm_pack_w4_bytes(int K, int N, int group) {
@@ -988,6 +1055,54 @@ tm_status tm_gemm_w4a16_grouped(const void* A, const tm_packed_w4* packed, const
   args.a_ks = K / 64;
   args.trace = g_trace;
   return launch_sk<true, OUT_ACT>(A, args, c, static_cast<cudaStream_t>(stream), UserWs{nullptr, 0}, &grp);
+}
+
+int64_t tm_attn_workspace_bytes(int B, int Hq, int Hkv, int Lmax) {
+  if (B <= 0 || Hq <= 0 || Hkv <= 0 || Lmax <= 0 || Hq % Hkv) return TM_ERR_INVALID_ARG;
+  const int G = Hq / Hkv;
+  if ((G & (G - 1)) || G > 8 || Lmax % kAttnMT) return TM_ERR_UNSUPPORTED_SHAPE;
+  const long long splits = (Lmax + kAttnSplit - 1) / kAttnSplit;
+  if (splits == 1) return 0;
+  return static_cast<int64_t>(ws_flag_bytes(B * Hkv)) + static_cast<int64_t>(B) * Hkv * splits * G * (kAttnD + 2) * 4;
+}
+
+
+tm_status tm_attn_decode_kv8(const void* Q, const void* k_codes, const void* v_codes, const void* k_sz,
+                             const void* v_sz, const int32_t* seq_lens, void* O, int B, int Hq, int Hkv, int Lmax,
+                             float softmax_scale, int q_dtype, void* workspace, int64_t workspace_bytes,
+                             void* stream) {
+  if (!Q || !k_codes || !v_codes || !k_sz || !v_sz || !seq_lens || !O) return TM_ERR_INVALID_ARG;
+  if (q_dtype != TM_DTYPE_BF16 && q_dtype != TM_DTYPE_FP16) return TM_ERR_INVALID_ARG;
+  const int64_t need = tm_attn_workspace_bytes(B, Hq, Hkv, Lmax);
+  if (need < 0) return static_cast<tm_status>(need);
+  if (need > 0 && (!workspace || workspace_bytes < need)) return TM_ERR_INVALID_ARG;
+  if (!aligned16(Q) || !aligned16(k_codes) || !aligned16(v_codes) || !aligned16(k_sz) || !aligned16(v_sz) ||
+      !aligned16(O) || (workspace && !aligned16(workspace)))
+    return TM_ERR_MISALIGNED;
+  const long long rows = static_cast<long long>(B) * Hkv * Lmax;
+  if (rows >= (1ll << 31)) return TM_ERR_UNSUPPORTED_SHAPE;
+  CUtensorMap mk, mv;
+  tm_status st = kv_tensor_map(k_codes, rows, &mk);
+  if (st != TM_OK) return st;
+  st = kv_tensor_map(v_codes, rows, &mv);
+  if (st != TM_OK) return st;
+  AttnArgs a;
+  a.q = static_cast<const uint16_t*>(Q);
+  a.ksz = static_cast<const uint32_t*>(k_sz);
+  a.vsz = static_cast<const uint32_t*>(v_sz);
+  a.seq_lens = seq_lens;
+  a.out = static_cast<uint16_t*>(O);
+  a.B = B;
+  a.Hq = Hq;
+  a.Hkv = Hkv;
+  a.Lmax = Lmax;
+  a.splits = (Lmax + kAttnSplit - 1) / kAttnSplit;
+  a.scale_log2 = softmax_scale * 1.4426950408889634f;
+  a.counters = need > 0 ? static_cast<int*>(workspace) : nullptr;
+  a.part = need > 0 ? reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + ws_flag_bytes(B * Hkv)) : nullptr;
+  const int G = Hq / Hkv;
+  auto s = static_cast<cudaStream_t>(stream);
+  return q_dtype == TM_DTYPE_BF16 ? launch_attn<true>(G, mk, mv, a, s) : launch_attn<false>(G, mk, mv, a, s);
 }
 
 tm_status tm_tp_finalize(const float* in_f32, void* out_bf16, int64_t count, void* stream) {

@@ -1,0 +1,341 @@
+// attn_dec.cuh -- low-bit-KV decode attention for sm_100a (§8(f) NEXT-2): the paper's attention
+// pipeline (§3.4 "Attention pipeline") for one decode step over an 8-bit KV cache.
+//
+//   S[t][h] = scale * Q[h] . K[t],  P = softmax_t(S),  O[h] = sum_t P[t][h] V[t]
+//   K[t] = (kq[t] - kz[t]) ks[t],   V[t] = (vq[t] - vz[t]) vs[t]   (one (scale, zero) per token, KV head)
+//
+// Pipeline (one CTA = one (sequence, KV head, 256-token split); 4 warps):
+//  * KV loading (§4.4): the CTA's four 64-token macro-tiles of K and V codes arrive by
+//    TMA (2-D, SWIZZLE_128B, one request per tile and tensor) plus 1-D bulk copies of their
+//    (scale, zero) words, all issued up front against one mbarrier per macro-tile, so the whole
+//    split is in flight at once; each warp then works on its 16-token micro-tile of every
+//    macro-tile as soon as that tile lands.
+//  * Q x K^T on the tensor core with the codes as the operand (§4.2 "adaptive head alignment",
+//    Alg. 1): mma.sync m16n8k16, A = 16 tokens x 16 channels of K, B = the
+//    G query heads of this KV head (grouped-query attention, G <= 8 = the MMA's N).  A lane loads
+//    16 contiguous code bytes of a token row with one LDS.128 and turns each byte pair into the
+//    exact fp16 pair (1024 + code) with one PRMT (I2F) -- so, as in the paper, Q is the
+//    operand that is rearranged: the B fragment of lane (g, c) for k-slice 4q + r holds
+//    Q[h][16(4q + c) + 4r .. +3], matching the K bytes that lane holds.  The zero point and scale
+//    are applied after the MMA in fp32:  S = ks (acc - (1024 + kz) sum_d Q[h][d]).
+//  * softmax streams over the micro-tiles (running max / sum per head, base 2), P is staged in
+//    shared memory scaled by vs, and P x V runs on the FMA pipe: lane l owns channels 4l .. 4l+3
+//    of every head; O = sum_t P'[t] (1024 + vq[t]) - sum_t P'[t] (1024 + vz[t]).
+//  * the four warps' partial states merge in shared memory; several splits of one sequence merge
+//    through a caller workspace (fixed split order, the last split to finish adds them:
+//    deterministic).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "ptx.cuh"
+
+namespace w4k {
+
+constexpr int kAttnD = 128;     // head dimension
+constexpr int kAttnMT = 64;     // tokens per macro-tile (PAPER Fig. 9)
+constexpr int kAttnTiles = 4;   // macro-tiles per CTA (256-token split)
+constexpr int kAttnSplit = kAttnMT * kAttnTiles;
+
+struct AttnArgs {
+  const uint16_t* q;        // [B][Hq][D] bf16 / fp16
+  const uint32_t* ksz;      // [B][Hkv][Lmax] (fp16 scale | fp16 zero << 16)
+  const uint32_t* vsz;
+  const int* seq_lens;      // [B]
+  uint16_t* out;            // [B][Hq][D]
+  float* part;              // [B][Hkv][splits][G][D + 2] (m, l, O) partials
+  int* counters;            // [B][Hkv], zero between launches
+  int B, Hq, Hkv, Lmax, splits;
+  float scale_log2;         // softmax scale * log2(e)
+};
+
+template <int G>
+struct AttnCfg {
+  static constexpr int KV_TILE = kAttnMT * kAttnD;          // bytes of one 8-bit macro-tile
+  static constexpr int SZ_TILE = kAttnMT * 4;
+  static constexpr int STAGE = (2 * KV_TILE + 2 * SZ_TILE + 1023) / 1024 * 1024;  // K, V, K sz, V sz (1 KB aligned: SW128)
+  static constexpr int OFF_TILES = 1024;
+  static constexpr int OFF_P = OFF_TILES + kAttnTiles * STAGE;          // per warp [16][8] P' + [8] alpha
+  static constexpr int P_BYTES = 4 * (16 * 8 + 8) * 4;
+  static constexpr int OFF_MERGE = OFF_P + P_BYTES;                     // per warp [G][D + 3]
+  static constexpr int MERGE_BYTES = 4 * G * (kAttnD + 4) * 4;
+  static constexpr int SMEM = OFF_MERGE + MERGE_BYTES + 1024;
+};
+
+__device__ __forceinline__ void hmma_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// bytes (b0, b1) of w at positions sel -> fp16 pair (1024 + b0, 1024 + b1), exact
+__device__ __forceinline__ uint32_t i2f_pair(uint32_t w, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(0x64646464u), "r"(sel));
+  return r;
+}
+
+__device__ __forceinline__ float f16lo(uint32_t x) { return __half2float(__ushort_as_half(static_cast<uint16_t>(x))); }
+__device__ __forceinline__ float f16hi(uint32_t x) {
+  return __half2float(__ushort_as_half(static_cast<uint16_t>(x >> 16)));
+}
+
+template <bool BF16>
+__device__ __forceinline__ float act_to_float(uint16_t x) {
+  if constexpr (BF16)
+    return __bfloat162float(__ushort_as_bfloat16(x));
+  else
+    return __half2float(__ushort_as_half(x));
+}
+
+template <int G, bool BF16>
+__global__ void __launch_bounds__(128)
+    attn_dec_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
+                    const AttnArgs args) {
+  using Cfg = AttnCfg<G>;
+  constexpr int D = kAttnD;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* const base_ptr = smem_raw + (base - raw);
+  const int split = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int L = args.seq_lens[b];
+  const int t0 = split * kAttnSplit;
+  if (t0 >= L) return;  // this split holds no tokens of the sequence
+  const int nsplit = (L + kAttnSplit - 1) / kAttnSplit;
+  const int ntiles = min(kAttnTiles, (L - t0 + kAttnMT - 1) / kAttnMT);
+  const long long row0 = (static_cast<long long>(b) * args.Hkv + hk) * args.Lmax + t0;  // cache row of token t0
+  const uint32_t bar = base;  // kAttnTiles mbarriers
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kAttnTiles; ++i) mbar_init(bar + 8 * i, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  grid_dependency_wait();  // the KV cache and Q may be written by the previous kernel
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ntiles; ++i) {
+      const uint32_t st = base + Cfg::OFF_TILES + i * Cfg::STAGE;
+      mbar_arrive_expect_tx(bar + 8 * i, 2 * Cfg::KV_TILE + 2 * Cfg::SZ_TILE);
+      const int r = static_cast<int>(row0 + i * kAttnMT);
+      tma_load_2d(st, &tmap_k, 0, r, bar + 8 * i);
+      tma_load_2d(st + Cfg::KV_TILE, &tmap_v, 0, r, bar + 8 * i);
+      bulk_g2s(st + 2 * Cfg::KV_TILE, args.ksz + row0 + i * kAttnMT, Cfg::SZ_TILE, bar + 8 * i);
+      bulk_g2s(st + 2 * Cfg::KV_TILE + Cfg::SZ_TILE, args.vsz + row0 + i * kAttnMT, Cfg::SZ_TILE, bar + 8 * i);
+    }
+  }
+
+  const int g = lane >> 2, c = lane & 3;
+  const int sig = (g >> 1) | ((g & 1) << 2);  // token row of MMA row g (conflict-free LDS.128)
+  const int h0 = hk * G;                      // first query head of this KV head
+  // ---- Q fragments (the rearrangement): slice 4q + r, lane (g = head, c): Q[g][16(4q + c) + 4r ..]
+  uint32_t qf[8][2];
+  {
+    const uint16_t* qh = args.q + (static_cast<size_t>(b) * args.Hq + h0 + (g < G ? g : 0)) * D;
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int d = 16 * (4 * q + c) + 4 * r;
+        float x[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[e] = g < G ? act_to_float<BF16>(qh[d + e]) : 0.f;
+        const __half2 lo = __floats2half2_rn(x[0], x[1]), hi = __floats2half2_rn(x[2], x[3]);
+        qf[4 * q + r][0] = *reinterpret_cast<const uint32_t*>(&lo);
+        qf[4 * q + r][1] = *reinterpret_cast<const uint32_t*>(&hi);
+      }
+  }
+  // sum_d Q[h][d] of the fp16 operand, for every head h < G (lane l sums channels 4l .. 4l+3)
+  float sq[G];
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    const uint16_t* qh = args.q + (static_cast<size_t>(b) * args.Hq + h0 + h) * D + 4 * lane;
+    float v = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v += __half2float(__float2half_rn(act_to_float<BF16>(qh[e])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    sq[h] = v;
+  }
+  float sq0 = 0.f, sq1 = 0.f;  // heads 2c, 2c + 1 of this lane (selects: no local-memory indexing)
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    sq0 = h == 2 * c ? sq[h] : sq0;
+    sq1 = h == 2 * c + 1 ? sq[h] : sq1;
+  }
+
+  // ---- per-warp streaming state: heads 2c, 2c + 1 (softmax), channels 4 lane .. +3 (output)
+  float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f}, c_run[2] = {0.f, 0.f};
+  float o[G][4];
+#pragma unroll
+  for (int h = 0; h < G; ++h)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[h][e] = 0.f;
+  float* const pw = reinterpret_cast<float*>(base_ptr + Cfg::OFF_P) + warp * (16 * 8 + 8);  // P'[16][8], alpha[8]
+
+  for (int i = 0; i < ntiles; ++i) {
+    const int tm = t0 + i * kAttnMT + 16 * warp;  // first token of this warp's micro-tile
+    if (tm >= L) break;
+    mbar_wait(bar + 8 * i, 0);
+    const uint8_t* st = base_ptr + Cfg::OFF_TILES + i * Cfg::STAGE;
+    const uint8_t* kt = st;
+    const uint8_t* vt = st + Cfg::KV_TILE;
+    const uint32_t* kz = reinterpret_cast<const uint32_t*>(st + 2 * Cfg::KV_TILE);
+    const uint32_t* vz = kz + kAttnMT;
+    // ---- S^T = K . Q^T for 16 tokens x 8 heads
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const int ra = 16 * warp + sig, rb = ra + 8;  // token rows of MMA rows g, g + 8
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int ch = 4 * q + c;  // 16-byte chunk of the row
+      const uint4 wa = *reinterpret_cast<const uint4*>(kt + ra * 128 + ((ch ^ (ra & 7)) << 4));
+      const uint4 wb = *reinterpret_cast<const uint4*>(kt + rb * 128 + ((ch ^ (rb & 7)) << 4));
+      const uint32_t xa[4] = {wa.x, wa.y, wa.z, wa.w}, xb[4] = {wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t a[4] = {i2f_pair(xa[r], 0x5140), i2f_pair(xb[r], 0x5140), i2f_pair(xa[r], 0x7362),
+                               i2f_pair(xb[r], 0x7362)};
+        hmma_f16(acc, a, qf[4 * q + r][0], qf[4 * q + r][1]);
+      }
+    }
+    // ---- scores (fold the zero point and scale back in, base-2 units), mask, streaming softmax
+    const uint32_t sza = kz[ra], szb = kz[rb];
+    const float ksa = f16lo(sza), kza = 1024.f + f16hi(sza), ksb = f16lo(szb), kzb = 1024.f + f16hi(szb);
+    const bool va = tm - 16 * warp + ra < L, vb = tm - 16 * warp + rb < L;
+    float s[4];
+    s[0] = va ? ksa * fmaf(-kza, sq0, acc[0]) * args.scale_log2 : -INFINITY;
+    s[1] = va ? ksa * fmaf(-kza, sq1, acc[1]) * args.scale_log2 : -INFINITY;
+    s[2] = vb ? ksb * fmaf(-kzb, sq0, acc[2]) * args.scale_log2 : -INFINITY;
+    s[3] = vb ? ksb * fmaf(-kzb, sq1, acc[3]) * args.scale_log2 : -INFINITY;
+    const uint32_t vsa = vz[ra], vsb = vz[rb];
+    const float vva = f16lo(vsa), vvb = f16lo(vsb);
+    const float vza = 1024.f + f16hi(vsa), vzb = 1024.f + f16hi(vsb);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {  // head 2c + j
+      float mx = fmaxf(s[j], s[2 + j]);
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      const float m_new = fmaxf(m_run[j], mx);
+      const float alpha = m_new == -INFINITY ? 1.f : exp2f(m_run[j] - m_new);
+      const float pa = m_new == -INFINITY ? 0.f : exp2f(s[j] - m_new);
+      const float pb = m_new == -INFINITY ? 0.f : exp2f(s[2 + j] - m_new);
+      float ps = pa + pb;
+      float pc = pa * vva * vza + pb * vvb * vzb;
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        ps += __shfl_xor_sync(0xffffffffu, ps, off);
+        pc += __shfl_xor_sync(0xffffffffu, pc, off);
+      }
+      m_run[j] = m_new;
+      l_run[j] = l_run[j] * alpha + ps;
+      c_run[j] = c_run[j] * alpha + pc;
+      pw[sig * 8 + 2 * c + j] = pa * vva;        // P'[token][head] = p * vs
+      pw[(sig + 8) * 8 + 2 * c + j] = pb * vvb;
+      if (g == 0) pw[128 + 2 * c + j] = alpha;
+    }
+    __syncwarp();
+    // ---- O += P' . (1024 + vq): lane owns channels 4 lane .. +3 of every head
+    {
+      float al[G];
+#pragma unroll
+      for (int h = 0; h < G; ++h) al[h] = pw[128 + h];
+#pragma unroll
+      for (int h = 0; h < G; ++h)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[h][e] *= al[h];
+      const int chl = lane >> 2, off = (lane & 3) * 4;
+#pragma unroll 4
+      for (int t = 0; t < 16; ++t) {
+        const int row = 16 * warp + t;
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(vt + row * 128 + ((chl ^ (row & 7)) << 4) + off);
+        const uint32_t p01 = i2f_pair(w, 0x5140), p23 = i2f_pair(w, 0x7362);
+        const float v[4] = {f16lo(p01), f16hi(p01), f16lo(p23), f16hi(p23)};
+        const float* pr = pw + t * 8;
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+          const float ph = pr[h];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o[h][e] = fmaf(ph, v[e], o[h][e]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // ---- merge the four warps: (m, l, O - corr) per head, fixed warp order
+  float* mg = reinterpret_cast<float*>(base_ptr + Cfg::OFF_MERGE) + warp * G * (D + 4);
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    const float ch = __shfl_sync(0xffffffffu, c_run[h & 1], h >> 1);  // corr of head h: lane (g = 0, c = h / 2)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) mg[h * (D + 4) + 4 * lane + e] = o[h][e] - ch;
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (2 * c + j < G) {
+        mg[(2 * c + j) * (D + 4) + D] = m_run[j];
+        mg[(2 * c + j) * (D + 4) + D + 1] = l_run[j];
+      }
+  }
+  __syncthreads();
+  const float* mall = reinterpret_cast<const float*>(base_ptr + Cfg::OFF_MERGE);
+  // thread layout for the output: G heads x 128 channels over 128 threads
+  for (int idx = threadIdx.x; idx < G * D; idx += 128) {
+    const int h = idx / D, d = idx - (idx / D) * D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, mall[(w * G + h) * (D + 4) + D]);
+    float Lsum = 0.f, O = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float mw = mall[(w * G + h) * (D + 4) + D];
+      const float f = mw == -INFINITY ? 0.f : exp2f(mw - M);
+      Lsum += f * mall[(w * G + h) * (D + 4) + D + 1];
+      O += f * mall[(w * G + h) * (D + 4) + d];
+    }
+    const size_t oidx = (static_cast<size_t>(b) * args.Hq + h0 + h) * D + d;
+    if (nsplit == 1) {
+      const float y = O / Lsum;
+      args.out[oidx] = BF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(y)) : __half_as_ushort(__float2half_rn(y));
+    } else {
+      float* pp = args.part + ((static_cast<size_t>(b) * args.Hkv + hk) * args.splits + split) * G * (D + 2) + h * (D + 2);
+      pp[d] = O;
+      if (d == 0) {
+        pp[D] = M;
+        pp[D + 1] = Lsum;
+      }
+    }
+  }
+  if (nsplit == 1) return;
+  // ---- split merge: the last split of (b, hk) to finish adds all splits in split order
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(args.counters + b * args.Hkv + hk, 1) == nsplit - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int idx = threadIdx.x; idx < G * D; idx += 128) {
+    const int h = idx / D, d = idx - (idx / D) * D;
+    const float* p0 = args.part + (static_cast<size_t>(b) * args.Hkv + hk) * args.splits * G * (D + 2) + h * (D + 2);
+    float M = -INFINITY;
+    for (int s = 0; s < nsplit; ++s) M = fmaxf(M, __ldcg(p0 + s * G * (D + 2) + D));
+    float Lsum = 0.f, O = 0.f;
+    for (int s = 0; s < nsplit; ++s) {
+      const float* ps = p0 + s * G * (D + 2);
+      const float ms = __ldcg(ps + D);
+      const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
+      Lsum += f * __ldcg(ps + D + 1);
+      O += f * __ldcg(ps + d);
+    }
+    const float y = O / Lsum;
+    args.out[(static_cast<size_t>(b) * args.Hq + h0 + h) * D + d] =
+        BF16 ? __bfloat16_as_ushort(__float2bfloat16_rn(y)) : __half_as_ushort(__float2half_rn(y));
+  }
+  if (threadIdx.x == 0) args.counters[b * args.Hkv + hk] = 0;  // zero for the next launch
+}
+
+}  // namespace w4k
