@@ -787,7 +787,7 @@ tm_status launch_attn_t(const CUtensorMap& mk, const CUtensorMap& mv, const Attn
   if (st != TM_OK) return st;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.splits, a.Hkv, a.B);
-  cfg.blockDim = dim3(128, 1, 1);
+  cfg.blockDim = dim3(kAttnThreads, 1, 1);
   cfg.dynamicSmemBytes = AttnCfg<G>::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attrs[1];

@@ -36,8 +36,17 @@ namespace w4k {
 
 constexpr int kAttnD = 128;     // head dimension
 constexpr int kAttnMT = 64;     // tokens per macro-tile (PAPER Fig. 9)
-constexpr int kAttnTiles = 4;   // macro-tiles per CTA (256-token split)
+#ifndef TM_ATTN_TILES
+#define TM_ATTN_TILES 4
+#endif
+constexpr int kAttnTiles = TM_ATTN_TILES;  // macro-tiles per CTA (4: 256-token split)
 constexpr int kAttnSplit = kAttnMT * kAttnTiles;
+#ifndef TM_ATTN_WARPS
+#define TM_ATTN_WARPS 8
+#endif
+constexpr int kAttnWarps = TM_ATTN_WARPS;     // 4 or 8: warp w takes micro-tile w % 4 of the macro-tiles
+                                              // i = w / 4 (mod kAttnWarps / 4)
+constexpr int kAttnThreads = 32 * kAttnWarps;
 
 struct AttnArgs {
   const uint16_t* q;        // [B][Hq][D] bf16 / fp16
@@ -58,9 +67,9 @@ struct AttnCfg {
   static constexpr int STAGE = (2 * KV_TILE + 2 * SZ_TILE + 1023) / 1024 * 1024;  // K, V, K sz, V sz (1 KB aligned: SW128)
   static constexpr int OFF_TILES = 1024;
   static constexpr int OFF_P = OFF_TILES + kAttnTiles * STAGE;          // per warp [16][8] P' + [8] alpha
-  static constexpr int P_BYTES = 4 * (16 * 8 + 8) * 4;
+  static constexpr int P_BYTES = kAttnWarps * (16 * 8 + 8) * 4;
   static constexpr int OFF_MERGE = OFF_P + P_BYTES;                     // per warp [G][D + 3]
-  static constexpr int MERGE_BYTES = 4 * G * (kAttnD + 4) * 4;
+  static constexpr int MERGE_BYTES = kAttnWarps * G * (kAttnD + 4) * 4;
   static constexpr int SMEM = OFF_MERGE + MERGE_BYTES + 1024;
 };
 
@@ -91,7 +100,7 @@ __device__ __forceinline__ float act_to_float(uint16_t x) {
 }
 
 template <int G, bool BF16>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kAttnThreads)
     attn_dec_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                     const AttnArgs args) {
   using Cfg = AttnCfg<G>;
@@ -116,8 +125,11 @@ __global__ void __launch_bounds__(128)
   }
   __syncthreads();
   grid_dependency_wait();  // the KV cache and Q may be written by the previous kernel
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < ntiles; ++i) {
+  // macro-tile i is requested by lane 0 of warp i (a bulk/TMA request costs its issuing thread
+  // ~300 cycles: four issuers put the whole split in flight four times sooner)
+  if (lane == 0 && warp < ntiles) {
+    {
+      const int i = warp;
       const uint32_t st = base + Cfg::OFF_TILES + i * Cfg::STAGE;
       mbar_arrive_expect_tx(bar + 8 * i, 2 * Cfg::KV_TILE + 2 * Cfg::SZ_TILE);
       const int r = static_cast<int>(row0 + i * kAttnMT);
@@ -169,15 +181,17 @@ __global__ void __launch_bounds__(128)
 
   // ---- per-warp streaming state: heads 2c, 2c + 1 (softmax), channels 4 lane .. +3 (output)
   float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f}, c_run[2] = {0.f, 0.f};
-  float o[G][4];
+  float o[8][4];  // P.V accumulators, tile 2P + u: (channel row g | g + 8) x (head 2c | 2c + 1)
 #pragma unroll
-  for (int h = 0; h < G; ++h)
+  for (int tt = 0; tt < 8; ++tt)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) o[h][e] = 0.f;
+    for (int e = 0; e < 4; ++e) o[tt][e] = 0.f;
   float* const pw = reinterpret_cast<float*>(base_ptr + Cfg::OFF_P) + warp * (16 * 8 + 8);  // P'[16][8], alpha[8]
 
-  for (int i = 0; i < ntiles; ++i) {
-    const int tm = t0 + i * kAttnMT + 16 * warp;  // first token of this warp's micro-tile
+  const int mtw = warp & 3;  // micro-tile of this warp in each of its macro-tiles
+  float al2[2];
+  for (int i = warp >> 2; i < ntiles; i += kAttnWarps / 4) {
+    const int tm = t0 + i * kAttnMT + 16 * mtw;  // first token of this warp's micro-tile
     if (tm >= L) break;
     mbar_wait(bar + 8 * i, 0);
     const uint8_t* st = base_ptr + Cfg::OFF_TILES + i * Cfg::STAGE;
@@ -186,8 +200,8 @@ __global__ void __launch_bounds__(128)
     const uint32_t* kz = reinterpret_cast<const uint32_t*>(st + 2 * Cfg::KV_TILE);
     const uint32_t* vz = kz + kAttnMT;
     // ---- S^T = K . Q^T for 16 tokens x 8 heads
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    const int ra = 16 * warp + sig, rb = ra + 8;  // token rows of MMA rows g, g + 8
+    float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc1[4] = {0.f, 0.f, 0.f, 0.f};  // two MMA chains
+    const int ra = 16 * mtw + sig, rb = ra + 8;  // token rows of MMA rows g, g + 8
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const int ch = 4 * q + c;  // 16-byte chunk of the row
@@ -198,13 +212,18 @@ __global__ void __launch_bounds__(128)
       for (int r = 0; r < 4; ++r) {
         const uint32_t a[4] = {i2f_pair(xa[r], 0x5140), i2f_pair(xb[r], 0x5140), i2f_pair(xa[r], 0x7362),
                                i2f_pair(xb[r], 0x7362)};
-        hmma_f16(acc, a, qf[4 * q + r][0], qf[4 * q + r][1]);
+        if (q == 0)
+          hmma_f16(acc, a, qf[4 * q + r][0], qf[4 * q + r][1]);
+        else
+          hmma_f16(acc1, a, qf[4 * q + r][0], qf[4 * q + r][1]);
       }
     }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[e] += acc1[e];
     // ---- scores (fold the zero point and scale back in, base-2 units), mask, streaming softmax
     const uint32_t sza = kz[ra], szb = kz[rb];
     const float ksa = f16lo(sza), kza = 1024.f + f16hi(sza), ksb = f16lo(szb), kzb = 1024.f + f16hi(szb);
-    const bool va = tm - 16 * warp + ra < L, vb = tm - 16 * warp + rb < L;
+    const bool va = tm - 16 * mtw + ra < L, vb = tm - 16 * mtw + rb < L;
     float s[4];
     s[0] = va ? ksa * fmaf(-kza, sq0, acc[0]) * args.scale_log2 : -INFINITY;
     s[1] = va ? ksa * fmaf(-kza, sq1, acc[1]) * args.scale_log2 : -INFINITY;
@@ -222,8 +241,10 @@ __global__ void __launch_bounds__(128)
       const float alpha = m_new == -INFINITY ? 1.f : exp2f(m_run[j] - m_new);
       const float pa = m_new == -INFINITY ? 0.f : exp2f(s[j] - m_new);
       const float pb = m_new == -INFINITY ? 0.f : exp2f(s[2 + j] - m_new);
+      // P' = p vs, rounded once to the fp16 MMA operand; the zero-point term uses the same values
+      const __half qa = __float2half_rn(pa * vva), qb = __float2half_rn(pb * vvb);
       float ps = pa + pb;
-      float pc = pa * vva * vza + pb * vvb * vzb;
+      float pc = __half2float(qa) * vza + __half2float(qb) * vzb;
 #pragma unroll
       for (int off = 4; off < 32; off <<= 1) {
         ps += __shfl_xor_sync(0xffffffffu, ps, off);
@@ -232,46 +253,67 @@ __global__ void __launch_bounds__(128)
       m_run[j] = m_new;
       l_run[j] = l_run[j] * alpha + ps;
       c_run[j] = c_run[j] * alpha + pc;
-      pw[sig * 8 + 2 * c + j] = pa * vva;        // P'[token][head] = p * vs
-      pw[(sig + 8) * 8 + 2 * c + j] = pb * vvb;
-      if (g == 0) pw[128 + 2 * c + j] = alpha;
+      __half* pt = reinterpret_cast<__half*>(pw);  // P'^T [8 heads][16 tokens] fp16
+      pt[(2 * c + j) * 16 + sig] = qa;
+      pt[(2 * c + j) * 16 + sig + 8] = qb;
+      al2[j] = alpha;
     }
     __syncwarp();
-    // ---- O += P' . (1024 + vq): lane owns channels 4 lane .. +3 of every head
+    // ---- O^T += V^T . P' on the tensor core: D[channel][head], A = V codes transposed (16
+    // channels x 16 tokens, exact fp16 1024 + code), B = P'^T^T (16 tokens x 8 heads, fp16).
+    // Lane (g, c) loads tokens 4c .. 4c + 3 of channels 32 P + 4g .. +3 (one LDS.32 each) and
+    // transposes the 4 x 4 bytes with PRMT: channel 32 P + 4g + e feeds row g (e = 0, 2) or row
+    // g + 8 (e = 1, 3) of tile 2P + e / 2; k-slots (2c, 2c + 1, 2c + 8, 2c + 9) are tokens
+    // 4c .. 4c + 3 in both operands.  Each lane accumulates its heads 2c, 2c + 1.
     {
-      float al[G];
 #pragma unroll
-      for (int h = 0; h < G; ++h) al[h] = pw[128 + h];
+      for (int tt = 0; tt < 8; ++tt) {
+        o[tt][0] *= al2[0];
+        o[tt][1] *= al2[1];
+        o[tt][2] *= al2[0];
+        o[tt][3] *= al2[1];
+      }
+      const uint2 pb2 = *reinterpret_cast<const uint2*>(reinterpret_cast<const __half*>(pw) + g * 16 + 4 * c);
 #pragma unroll
-      for (int h = 0; h < G; ++h)
+      for (int P = 0; P < 4; ++P) {
+        const int cb = 32 * P + 4 * g;  // first channel of this lane's 4
+        uint32_t r[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) o[h][e] *= al[h];
-      const int chl = lane >> 2, off = (lane & 3) * 4;
-#pragma unroll 4
-      for (int t = 0; t < 16; ++t) {
-        const int row = 16 * warp + t;
-        const uint32_t w = *reinterpret_cast<const uint32_t*>(vt + row * 128 + ((chl ^ (row & 7)) << 4) + off);
-        const uint32_t p01 = i2f_pair(w, 0x5140), p23 = i2f_pair(w, 0x7362);
-        const float v[4] = {f16lo(p01), f16hi(p01), f16lo(p23), f16hi(p23)};
-        const float* pr = pw + t * 8;
+        for (int i = 0; i < 4; ++i) {
+          const int row = 16 * mtw + 4 * c + i;
+          r[i] = *reinterpret_cast<const uint32_t*>(vt + row * 128 + (((cb >> 4) ^ (row & 7)) << 4) + (cb & 15));
+        }
+        uint32_t pr[4][2];  // channel e: fp16 pairs (tokens 4c, 4c+1), (4c+2, 4c+3)
 #pragma unroll
-        for (int h = 0; h < G; ++h) {
-          const float ph = pr[h];
+        for (int e = 0; e < 4; ++e) {
+          uint32_t x01, x23;
+          asm("prmt.b32 %0, %1, %2, %3;" : "=r"(x01) : "r"(r[0]), "r"(r[1]), "r"(e | ((4 + e) << 4)));
+          asm("prmt.b32 %0, %1, %2, %3;" : "=r"(x23) : "r"(r[2]), "r"(r[3]), "r"(e | ((4 + e) << 4)));
+          pr[e][0] = i2f_pair(x01, 0x5140);
+          pr[e][1] = i2f_pair(x23, 0x5140);
+        }
 #pragma unroll
-          for (int e = 0; e < 4; ++e) o[h][e] = fmaf(ph, v[e], o[h][e]);
+        for (int u = 0; u < 2; ++u) {  // tile 2P + u: rows g <- channel e = 2u, g + 8 <- e = 2u + 1
+          const uint32_t afr[4] = {pr[2 * u][0], pr[2 * u + 1][0], pr[2 * u][1], pr[2 * u + 1][1]};
+          hmma_f16(o[2 * P + u], afr, pb2.x, pb2.y);
         }
       }
     }
     __syncwarp();
   }
-  // ---- merge the four warps: (m, l, O - corr) per head, fixed warp order
+  // ---- merge the warps: (m, l, O - corr) per head, fixed warp order
   float* mg = reinterpret_cast<float*>(base_ptr + Cfg::OFF_MERGE) + warp * G * (D + 4);
 #pragma unroll
-  for (int h = 0; h < G; ++h) {
-    const float ch = __shfl_sync(0xffffffffu, c_run[h & 1], h >> 1);  // corr of head h: lane (g = 0, c = h / 2)
+  for (int P = 0; P < 4; ++P)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) mg[h * (D + 4) + 4 * lane + e] = o[h][e] - ch;
-  }
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (2 * c + j < G) {
+          const int ch = 32 * P + 4 * g + 2 * u;  // channel of row g; row g + 8 is ch + 1
+          mg[(2 * c + j) * (D + 4) + ch] = o[2 * P + u][j] - c_run[j];
+          mg[(2 * c + j) * (D + 4) + ch + 1] = o[2 * P + u][2 + j] - c_run[j];
+        }
   if (g == 0) {
 #pragma unroll
     for (int j = 0; j < 2; ++j)
@@ -283,14 +325,14 @@ __global__ void __launch_bounds__(128)
   __syncthreads();
   const float* mall = reinterpret_cast<const float*>(base_ptr + Cfg::OFF_MERGE);
   // thread layout for the output: G heads x 128 channels over 128 threads
-  for (int idx = threadIdx.x; idx < G * D; idx += 128) {
+  for (int idx = threadIdx.x; idx < G * D; idx += kAttnThreads) {
     const int h = idx / D, d = idx - (idx / D) * D;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, mall[(w * G + h) * (D + 4) + D]);
+    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, mall[(w * G + h) * (D + 4) + D]);
     float Lsum = 0.f, O = 0.f;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
+    for (int w = 0; w < kAttnWarps; ++w) {
       const float mw = mall[(w * G + h) * (D + 4) + D];
       const float f = mw == -INFINITY ? 0.f : exp2f(mw - M);
       Lsum += f * mall[(w * G + h) * (D + 4) + D + 1];
@@ -318,18 +360,34 @@ __global__ void __launch_bounds__(128)
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int idx = threadIdx.x; idx < G * D; idx += 128) {
+  for (int idx = threadIdx.x; idx < G * D; idx += kAttnThreads) {
     const int h = idx / D, d = idx - (idx / D) * D;
     const float* p0 = args.part + (static_cast<size_t>(b) * args.Hkv + hk) * args.splits * G * (D + 2) + h * (D + 2);
-    float M = -INFINITY;
-    for (int s = 0; s < nsplit; ++s) M = fmaxf(M, __ldcg(p0 + s * G * (D + 2) + D));
-    float Lsum = 0.f, O = 0.f;
-    for (int s = 0; s < nsplit; ++s) {
-      const float* ps = p0 + s * G * (D + 2);
-      const float ms = __ldcg(ps + D);
-      const float f = ms == -INFINITY ? 0.f : exp2f(ms - M);
-      Lsum += f * __ldcg(ps + D + 1);
-      O += f * __ldcg(ps + d);
+    // all of a thread's loads are issued before they are combined (L2 latency paid once per 8)
+    float M = -INFINITY, Lsum = 0.f, O = 0.f;
+    for (int s0 = 0; s0 < nsplit; s0 += 8) {
+      float ms[8], ls[8], os[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float* ps = p0 + (s0 + j) * G * (D + 2);
+        const bool ok = s0 + j < nsplit;
+        ms[j] = ok ? __ldcg(ps + D) : -INFINITY;
+        ls[j] = ok ? __ldcg(ps + D + 1) : 0.f;
+        os[j] = ok ? __ldcg(ps + d) : 0.f;
+      }
+      float mb = M;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) mb = fmaxf(mb, ms[j]);
+      const float fo = M == -INFINITY ? 0.f : exp2f(M - mb);  // rescale the running sums (split order kept)
+      Lsum *= fo;
+      O *= fo;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float f = ms[j] == -INFINITY ? 0.f : exp2f(ms[j] - mb);
+        Lsum += f * ls[j];
+        O += f * os[j];
+      }
+      M = mb;
     }
     const float y = O / Lsum;
     args.out[(static_cast<size_t>(b) * args.Hq + h0 + h) * D + d] =

@@ -1,0 +1,22 @@
+"""One decode-attention shape a few times (for ncu).  python scripts/attn_prof_one.py B L"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2508_15601_b200 import api  # noqa: E402
+
+B, L = int(sys.argv[1]), int(sys.argv[2])
+Hq, Hkv, D = 32, 8, 128
+kc = torch.randint(0, 256, (B, Hkv, L, D), dtype=torch.uint8, device="cuda")
+vc = torch.randint(0, 256, (B, Hkv, L, D), dtype=torch.uint8, device="cuda")
+sc = (torch.rand(B, Hkv, L, device="cuda") * 0.02 + 0.01).half()
+zz = torch.full((B, Hkv, L), 128.0, device="cuda").half()
+ks = api.pack_kv_sz(sc, zz)
+Q = torch.randn(B, Hq, D, device="cuda").to(torch.bfloat16)
+sl = torch.full((B,), L, dtype=torch.int32, device="cuda")
+ws = api.attn_workspace(B, Hq, Hkv, L)
+for _ in range(4):
+    api.attn_decode_kv8(Q, kc, vc, ks, ks, sl, workspace=ws)
+torch.cuda.synchronize()
