@@ -328,6 +328,37 @@ def moe_leg(stream, reps=20):
                 grouped_frac_of_hbm=round(nbytes / tg / 1e9 / load_peaks()["hbm"], 4))
 
 
+def attention_leg(stream, reps=20, B=32, L=8192):
+    """Context leg (§8(f) NEXT-2): one decode step of 8-bit-KV attention with Llama-3-8B heads
+    (Hq 32, Hkv 8, D 128), B sequences of L cached tokens, two caches rotating (1.1 GB > L2).
+    GB/s = KV codes + (scale, zero) words + Q + O bytes / time."""
+    import torch
+    from paper_2508_15601_b200 import api
+    Hq, Hkv, D = 32, 8, 128
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    sets = []
+    for _ in range(2):
+        kc = torch.randint(0, 256, (B, Hkv, L, D), dtype=torch.uint8, device="cuda", generator=g)
+        vc = torch.randint(0, 256, (B, Hkv, L, D), dtype=torch.uint8, device="cuda", generator=g)
+        sc = (torch.rand(B, Hkv, L, device="cuda", generator=g) * 0.02 + 0.01).half()
+        zz = torch.full((B, Hkv, L), 128.0, device="cuda").half()
+        sets.append((kc, vc, api.pack_kv_sz(sc, zz), api.pack_kv_sz(sc, zz)))
+    Q = torch.randn(B, Hq, D, device="cuda", generator=g).to(torch.bfloat16)
+    sl = torch.full((B,), L, dtype=torch.int32, device="cuda")
+    ws = api.attn_workspace(B, Hq, Hkv, L)
+    O = torch.empty_like(Q)
+    gr = capture(lambda: [api.attn_decode_kv8(Q, *sets[i % 2][:2], *sets[i % 2][2:], sl, workspace=ws, out=O)
+                          for i in range(reps)], stream)
+    t = time_graph(gr, 3, stream) / 3 / reps
+    nbytes = B * Hkv * L * (2 * D + 8) + 2 * B * Hq * D * 2
+    del sets
+    torch.cuda.empty_cache()
+    return dict(workload=f"decode attention, 8-bit KV cache, Hq=32 Hkv=8 D=128, B={B} L={L}, bf16 Q/O",
+                us=round(t * 1e6, 2), GBps=round(nbytes / t / 1e9, 1),
+                frac_of_hbm=round(nbytes / t / 1e9 / load_peaks()["hbm"], 4))
+
+
 def ncu_traffic(ms, L):
     """Per-launch DRAM traffic of the GEMM kernel from the committed ncu capture, if present."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -516,6 +547,7 @@ def bench_ours(args):
                           peak_source=f"MEASURED_PEAKS.json bf16_tflops ({peaks['src']}, burst: cuBLAS bf16 8192^3)"))
     if world == 1 and not args.no_prefill:
         res["moe"] = moe_leg(stream)
+        res["attention"] = attention_leg(stream)
     if world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline()
     print(json.dumps(res), flush=True)

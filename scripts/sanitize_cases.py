@@ -24,7 +24,7 @@ cases = [  # (M, N, K, group, decode_cluster_force, (tile, split) override)
 ok = True
 only = os.environ.get("SAN_ONLY")
 for i, (M, N, K, g, force, (tile, split)) in enumerate(cases):
-    if only is not None and i != int(only):
+    if only is not None and (only == "extra" or i != int(only)):
         continue
     api.set_decode_cluster(force)
     api.set_gemm_override(tile, split)
@@ -41,4 +41,48 @@ for i, (M, N, K, g, force, (tile, split)) in enumerate(cases):
     ok &= r["ok"]
     api.set_decode_cluster(0)
     api.set_gemm_override(0, 0)
+if only is None or only == "extra":
+    # round-2 kernels: grouped MoE decode, W8A16 bit planes, AWQ/GPTQ converters, decode attention
+    from oracle import formats as F
+    from oracle.attention import decode_attention_f64
+    from oracle.moe import grouped_gemm_f64
+    m = [3, 0, 5, 2]
+    ds = [synth.awq_like(1, 256, 512, seed=50 + e) for e in range(4)]
+    qs = [dd["q"] for dd in ds]
+    s4 = np.stack([dd["s"] for dd in ds])
+    z4 = np.stack([dd["z"] for dd in ds])
+    A = synth.awq_like(10, 256, 512, seed=60)["A"]
+    pe = api.pack_experts([torch.from_numpy(q).cuda() for q in qs], torch.from_numpy(s4).cuda(),
+                          torch.from_numpy(z4).cuda(), 128)
+    C = api.gemm_w4a16_grouped(torch.from_numpy(A).to(torch.bfloat16).cuda(), pe, torch.from_numpy(s4).cuda(),
+                               torch.from_numpy(z4).cuda(), m)
+    ref = grouped_gemm_f64(A, qs, s4, z4, 128, m)
+    ok &= compare.relfro(C.float().cpu().numpy(), ref) < 5e-3
+    print("grouped", ok, flush=True)
+    rng = np.random.default_rng(1)
+    q8 = rng.integers(0, 256, (512, 256), dtype=np.uint8)
+    s8 = rng.uniform(1e-3, 1e-2, (4, 256)).astype(np.float16)
+    z8 = rng.integers(0, 256, (4, 256))
+    pk, sp, zp = api.pack_w8(torch.from_numpy(q8).cuda(), torch.from_numpy(s8).cuda(),
+                             torch.from_numpy(z8.astype(np.float16)).cuda(), 128)
+    A8 = synth.awq_like(5, 256, 512, seed=61)["A"]
+    C8 = api.gemm_w8a16(torch.from_numpy(A8).to(torch.bfloat16).cuda(), pk, sp, zp)
+    ok &= compare.relfro(C8.float().cpu().numpy(), F.w8a16_gemm_f64(A8, q8, s8, z8, 128)) < 5e-3
+    print("w8", ok, flush=True)
+    dd = synth.uniform(1, 256, 512, group=128, seed=62)
+    pa, za = api.pack_awq(torch.from_numpy(F.awq_pack_cols(dd["q"])).cuda(),
+                          torch.from_numpy(F.awq_pack_cols(dd["z"].astype(np.uint8))).cuda(), 512, 256, 128)
+    gw, gz = F.gptq_pack(dd["q"], np.clip(dd["z"].astype(np.int64), 1, 15))
+    pg, zg = api.pack_gptq(torch.from_numpy(gw).cuda(), torch.from_numpy(gz).cuda(), 512, 256, 128)
+    torch.cuda.synchronize()
+    print("converters", flush=True)
+    pr = synth.kv_decode_problem(2, 8, 2, 128, 576, [570, 9], 8, seed=63)
+    Q = torch.from_numpy(pr["Q"]).to(torch.bfloat16).cuda()
+    ks = api.pack_kv_sz(torch.from_numpy(pr["ks"]).cuda(), torch.from_numpy(pr["kz"]).cuda())
+    vs = api.pack_kv_sz(torch.from_numpy(pr["vs"]).cuda(), torch.from_numpy(pr["vz"]).cuda())
+    O = api.attn_decode_kv8(Q, torch.from_numpy(pr["kq"]).cuda(), torch.from_numpy(pr["vq"]).cuda(), ks, vs,
+                            torch.from_numpy(pr["seq_lens"]).cuda(), workspace=api.attn_workspace(2, 8, 2, 576))
+    refa = decode_attention_f64(pr["Q"], pr["kq"], pr["ks"], pr["kz"], pr["vq"], pr["vs"], pr["vz"], pr["seq_lens"])
+    ok &= compare.relfro(O.float().cpu().numpy(), refa) < 5e-3
+    print("attention", ok, flush=True)
 print("all ok" if ok else "FAILURES")
