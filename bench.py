@@ -222,6 +222,7 @@ def time_graph(graph, steps, stream):
 
 def capture(fn, stream):
     import torch
+    torch.cuda.synchronize()  # inputs made on the default stream are complete before `stream` reads them
     g = torch.cuda.CUDAGraph()
     with torch.cuda.stream(stream):
         with torch.cuda.graph(g, stream=stream):
@@ -463,6 +464,7 @@ def bench_ours(args):
     host_A = sets[0]["A_all"].cpu().pin_memory()
     host_C = torch.empty(sets[0]["C_all"].numel(), dtype=torch.bfloat16).pin_memory()
     stream = torch.cuda.Stream(device)
+    torch.cuda.synchronize()
     with torch.cuda.stream(stream):
         for _ in range(max(args.warmup, 3)):
             n_launch = run_step(layers, io, ms)

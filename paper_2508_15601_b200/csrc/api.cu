@@ -313,7 +313,9 @@ tm_status library_workspace(cudaStream_t stream, size_t need, void** out) {
       (void)cudaGetLastError();
       return TM_ERR_CUDA;
     }
-    if (cudaMemset(w.ptr, 0, alloc) != cudaSuccess) return TM_ERR_CUDA;
+    // zeroed in stream order: a cudaMemset on the legacy stream does not order against non-blocking
+    // streams, and the kernel reads the flags (measured: a stream-K launch on a fresh stream trapped)
+    if (cudaMemsetAsync(w.ptr, 0, alloc, stream) != cudaSuccess) return TM_ERR_CUDA;
     w.bytes = alloc;
   }
   *out = w.ptr;
@@ -779,6 +781,22 @@ int aux_grid(long long work, int block) {
 }  // namespace
 
 namespace {
+// tokens per attention CTA: split each (sequence, KV head) so the grid holds about two CTAs per
+// SM (each CTA streams its tokens through a ring of macro-tiles), at least 128 tokens each
+int attn_split_tokens(int B, int Hkv, int Lmax) {
+  const long long pairs = static_cast<long long>(B) * Hkv;
+  const long long target = 2ll * num_sms();
+  long long splits = (target + pairs - 1) / pairs;
+  if (splits < 1) splits = 1;
+  long long per = (Lmax + splits - 1) / splits;
+  per = ((per + kAttnMT - 1) / kAttnMT) * kAttnMT;
+  if (per < 128) per = 128;
+  if (per > Lmax) per = Lmax;
+  return static_cast<int>(per);
+}
+}  // namespace
+
+namespace {
 template <int G, bool BF16>
 tm_status launch_attn_t(const CUtensorMap& mk, const CUtensorMap& mv, const AttnArgs& a, cudaStream_t s) {
   auto kern = attn_dec_kernel<G, BF16>;
@@ -1061,7 +1079,7 @@ int64_t tm_attn_workspace_bytes(int B, int Hq, int Hkv, int Lmax) {
   if (B <= 0 || Hq <= 0 || Hkv <= 0 || Lmax <= 0 || Hq % Hkv) return TM_ERR_INVALID_ARG;
   const int G = Hq / Hkv;
   if ((G & (G - 1)) || G > 8 || Lmax % kAttnMT) return TM_ERR_UNSUPPORTED_SHAPE;
-  const long long splits = (Lmax + kAttnSplit - 1) / kAttnSplit;
+  const long long splits = (Lmax + attn_split_tokens(B, Hkv, Lmax) - 1) / attn_split_tokens(B, Hkv, Lmax);
   if (splits == 1) return 0;
   return static_cast<int64_t>(ws_flag_bytes(B * Hkv)) + static_cast<int64_t>(B) * Hkv * splits * G * (kAttnD + 2) * 4;
 }
@@ -1096,7 +1114,8 @@ tm_status tm_attn_decode_kv8(const void* Q, const void* k_codes, const void* v_c
   a.Hq = Hq;
   a.Hkv = Hkv;
   a.Lmax = Lmax;
-  a.splits = (Lmax + kAttnSplit - 1) / kAttnSplit;
+  a.split_tokens = attn_split_tokens(B, Hkv, Lmax);
+  a.splits = (Lmax + a.split_tokens - 1) / a.split_tokens;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
   a.counters = need > 0 ? static_cast<int*>(workspace) : nullptr;
   a.part = need > 0 ? reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + ws_flag_bytes(B * Hkv)) : nullptr;

@@ -4,12 +4,13 @@
 //   S[t][h] = scale * Q[h] . K[t],  P = softmax_t(S),  O[h] = sum_t P[t][h] V[t]
 //   K[t] = (kq[t] - kz[t]) ks[t],   V[t] = (vq[t] - vz[t]) vs[t]   (one (scale, zero) per token, KV head)
 //
-// Pipeline (one CTA = one (sequence, KV head, 256-token split); 4 warps):
-//  * KV loading (§4.4): the CTA's four 64-token macro-tiles of K and V codes arrive by
-//    TMA (2-D, SWIZZLE_128B, one request per tile and tensor) plus 1-D bulk copies of their
-//    (scale, zero) words, all issued up front against one mbarrier per macro-tile, so the whole
-//    split is in flight at once; each warp then works on its 16-token micro-tile of every
-//    macro-tile as soon as that tile lands.
+// Pipeline (one CTA = one (sequence, KV head, token split); 8 consumer + 2 producer warps):
+//  * KV loading (§4.4): 64-token macro-tiles of K and V codes stream through a
+//    4-stage shared-memory ring by TMA (2-D, SWIZZLE_128B) plus 1-D bulk copies of their (scale,
+//    zero) words; two producer warps (K, V) issue them, full/empty mbarriers hand the stages to
+//    two consumer groups of 4 warps (tile i -> group i % 2), each warp taking one 16-token
+//    micro-tile.  The host sizes the split so the grid holds ~2 CTAs per SM: long contexts are
+//    streamed by a few long-lived CTAs instead of many short ones.
 //  * Q x K^T on the tensor core with the codes as the operand (§4.2 "adaptive head alignment",
 //    Alg. 1): mma.sync m16n8k16, A = 16 tokens x 16 channels of K, B = the
 //    G query heads of this KV head (grouped-query attention, G <= 8 = the MMA's N).  A lane loads
@@ -39,14 +40,16 @@ constexpr int kAttnMT = 64;     // tokens per macro-tile (PAPER Fig. 9)
 #ifndef TM_ATTN_TILES
 #define TM_ATTN_TILES 4
 #endif
-constexpr int kAttnTiles = TM_ATTN_TILES;  // macro-tiles per CTA (4: 256-token split)
-constexpr int kAttnSplit = kAttnMT * kAttnTiles;
+constexpr int kAttnTiles = TM_ATTN_TILES;  // macro-tile ring depth (stages)
 #ifndef TM_ATTN_WARPS
 #define TM_ATTN_WARPS 8
 #endif
 constexpr int kAttnWarps = TM_ATTN_WARPS;     // 4 or 8: warp w takes micro-tile w % 4 of the macro-tiles
                                               // i = w / 4 (mod kAttnWarps / 4)
-constexpr int kAttnThreads = 32 * kAttnWarps;
+constexpr int kAttnThreads = 32 * (kAttnWarps + 2);  // + 2 producer warps (K tiles, V tiles)
+// a ring stage is always reused by the same consumer group (tile i -> group i % groups, stage
+// i % stages): a group can then never run a full ring lap ahead of the phase it waits for
+static_assert(kAttnTiles % (kAttnWarps / 4) == 0, "ring stages must be a multiple of the consumer groups");
 
 struct AttnArgs {
   const uint16_t* q;        // [B][Hq][D] bf16 / fp16
@@ -57,6 +60,7 @@ struct AttnArgs {
   float* part;              // [B][Hkv][splits][G][D + 2] (m, l, O) partials
   int* counters;            // [B][Hkv], zero between launches
   int B, Hq, Hkv, Lmax, splits;
+  int split_tokens;         // tokens per CTA (multiple of 64; host-chosen so the grid fills the GPU)
   float scale_log2;         // softmax scale * log2(e)
 };
 
@@ -111,33 +115,45 @@ __global__ void __launch_bounds__(kAttnThreads)
   uint8_t* const base_ptr = smem_raw + (base - raw);
   const int split = blockIdx.x, hk = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int L = args.seq_lens[b];
-  const int t0 = split * kAttnSplit;
+  // every input (KV cache, Q, seq_lens) may be written by the previous kernel on the stream: no
+  // global read before griddepcontrol.wait (PDL lets this grid start before that kernel ends)
+  grid_dependency_wait();
+  // (clamped to the cache capacity: a bad length must not index past the workspace sized for Lmax)
+  const int L = min(args.seq_lens[b], args.Lmax);
+  const int t0 = split * args.split_tokens;
   if (t0 >= L) return;  // this split holds no tokens of the sequence
-  const int nsplit = (L + kAttnSplit - 1) / kAttnSplit;
-  const int ntiles = min(kAttnTiles, (L - t0 + kAttnMT - 1) / kAttnMT);
+  const int nsplit = (L + args.split_tokens - 1) / args.split_tokens;
+  const int ntiles = min(args.split_tokens, L - t0 + kAttnMT - 1) / kAttnMT;
   const long long row0 = (static_cast<long long>(b) * args.Hkv + hk) * args.Lmax + t0;  // cache row of token t0
-  const uint32_t bar = base;  // kAttnTiles mbarriers
+  const uint32_t bar_full = base, bar_empty = base + 8 * kAttnTiles;  // ring of kAttnTiles macro-tiles
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kAttnTiles; ++i) mbar_init(bar + 8 * i, 1);
+    for (int i = 0; i < kAttnTiles; ++i) {
+      mbar_init(bar_full + 8 * i, 2);   // K producer + V producer
+      mbar_init(bar_empty + 8 * i, 4);  // the 4 warps of the tile's consumer group
+    }
     fence_mbar_init();
   }
   __syncthreads();
-  grid_dependency_wait();  // the KV cache and Q may be written by the previous kernel
-  // macro-tile i is requested by lane 0 of warp i (a bulk/TMA request costs its issuing thread
-  // ~300 cycles: four issuers put the whole split in flight four times sooner)
-  if (lane == 0 && warp < ntiles) {
-    {
-      const int i = warp;
-      const uint32_t st = base + Cfg::OFF_TILES + i * Cfg::STAGE;
-      mbar_arrive_expect_tx(bar + 8 * i, 2 * Cfg::KV_TILE + 2 * Cfg::SZ_TILE);
-      const int r = static_cast<int>(row0 + i * kAttnMT);
-      tma_load_2d(st, &tmap_k, 0, r, bar + 8 * i);
-      tma_load_2d(st + Cfg::KV_TILE, &tmap_v, 0, r, bar + 8 * i);
-      bulk_g2s(st + 2 * Cfg::KV_TILE, args.ksz + row0 + i * kAttnMT, Cfg::SZ_TILE, bar + 8 * i);
-      bulk_g2s(st + 2 * Cfg::KV_TILE + Cfg::SZ_TILE, args.vsz + row0 + i * kAttnMT, Cfg::SZ_TILE, bar + 8 * i);
+  if (warp >= kAttnWarps) {
+    // ---- producers (§4.4 KV loading pipeline): warp kAttnWarps streams K tiles + K (scale, zero)
+    // words, the next warp V; a bulk/TMA request costs its issuing thread ~300 cycles, so the
+    // two tensors get separate issuers
+    if (lane == 0) {
+      const bool isv = warp == kAttnWarps + 1;
+      for (int i = 0; i < ntiles; ++i) {
+        const int stg = i % kAttnTiles;
+        mbar_wait(bar_empty + 8 * stg, ((i / kAttnTiles) & 1) ^ 1);
+        const uint32_t st = base + Cfg::OFF_TILES + stg * Cfg::STAGE;
+        const uint32_t fb = bar_full + 8 * stg;
+        mbar_arrive_expect_tx(fb, Cfg::KV_TILE + Cfg::SZ_TILE);
+        const int r = static_cast<int>(row0 + i * kAttnMT);
+        tma_load_2d(st + (isv ? Cfg::KV_TILE : 0), isv ? &tmap_v : &tmap_k, 0, r, fb);
+        bulk_g2s(st + 2 * Cfg::KV_TILE + (isv ? Cfg::SZ_TILE : 0), (isv ? args.vsz : args.ksz) + row0 + i * kAttnMT,
+                 Cfg::SZ_TILE, fb);
+      }
     }
+    return;
   }
 
   const int g = lane >> 2, c = lane & 3;
@@ -192,9 +208,13 @@ __global__ void __launch_bounds__(kAttnThreads)
   float al2[2];
   for (int i = warp >> 2; i < ntiles; i += kAttnWarps / 4) {
     const int tm = t0 + i * kAttnMT + 16 * mtw;  // first token of this warp's micro-tile
-    if (tm >= L) break;
-    mbar_wait(bar + 8 * i, 0);
-    const uint8_t* st = base_ptr + Cfg::OFF_TILES + i * Cfg::STAGE;
+    const int stg = i % kAttnTiles;
+    if (tm >= L) {  // micro-tile past the sequence end (last tile): release the stage only
+      if (lane == 0) mbar_arrive(bar_empty + 8 * stg);
+      continue;
+    }
+    mbar_wait(bar_full + 8 * stg, (i / kAttnTiles) & 1);
+    const uint8_t* st = base_ptr + Cfg::OFF_TILES + stg * Cfg::STAGE;
     const uint8_t* kt = st;
     const uint8_t* vt = st + Cfg::KV_TILE;
     const uint32_t* kz = reinterpret_cast<const uint32_t*>(st + 2 * Cfg::KV_TILE);
@@ -300,6 +320,7 @@ __global__ void __launch_bounds__(kAttnThreads)
       }
     }
     __syncwarp();
+    if (lane == 0) mbar_arrive(bar_empty + 8 * stg);
   }
   // ---- merge the warps: (m, l, O - corr) per head, fixed warp order
   float* mg = reinterpret_cast<float*>(base_ptr + Cfg::OFF_MERGE) + warp * G * (D + 4);
@@ -322,10 +343,10 @@ __global__ void __launch_bounds__(kAttnThreads)
         mg[(2 * c + j) * (D + 4) + D + 1] = l_run[j];
       }
   }
-  __syncthreads();
+  asm volatile("bar.sync 1, %0;" ::"r"(32 * kAttnWarps) : "memory");  // consumers only
   const float* mall = reinterpret_cast<const float*>(base_ptr + Cfg::OFF_MERGE);
   // thread layout for the output: G heads x 128 channels over 128 threads
-  for (int idx = threadIdx.x; idx < G * D; idx += kAttnThreads) {
+  for (int idx = threadIdx.x; idx < G * D; idx += 32 * kAttnWarps) {
     const int h = idx / D, d = idx - (idx / D) * D;
     float M = -INFINITY;
 #pragma unroll
@@ -354,13 +375,15 @@ __global__ void __launch_bounds__(kAttnThreads)
   if (nsplit == 1) return;
   // ---- split merge: the last split of (b, hk) to finish adds all splits in split order
   __shared__ int last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(args.counters + b * args.Hkv + hk, 1) == nsplit - 1;
-  __syncthreads();
+  asm volatile("bar.sync 1, %0;" ::"r"(32 * kAttnWarps) : "memory");
+  if (threadIdx.x == 0) {
+    __threadfence();  // cumulative over the barrier: every consumer's partial stores
+    last = atomicAdd(args.counters + b * args.Hkv + hk, 1) == nsplit - 1;
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(32 * kAttnWarps) : "memory");
   if (!last) return;
   __threadfence();
-  for (int idx = threadIdx.x; idx < G * D; idx += kAttnThreads) {
+  for (int idx = threadIdx.x; idx < G * D; idx += 32 * kAttnWarps) {
     const int h = idx / D, d = idx - (idx / D) * D;
     const float* p0 = args.part + (static_cast<size_t>(b) * args.Hkv + hk) * args.splits * G * (D + 2) + h * (D + 2);
     // all of a thread's loads are issued before they are combined (L2 latency paid once per 8)

@@ -12,6 +12,7 @@ from paper_2508_15601_b200 import api  # noqa: E402
 
 def gtime(fn, reps=20):
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # inputs were made on the default stream
     with torch.cuda.stream(s):
         fn()
         torch.cuda.synchronize()

@@ -31,6 +31,7 @@ def make_sets(N, K, n):
 
 def time_graph(calls, reps=10):
     stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())  # inputs were made on the default stream
     with torch.cuda.stream(stream):
         for c in calls:
             c()

@@ -14,6 +14,7 @@ N, K, E, g = 14336, 4096, 8, 128
 
 def gtime(fn, reps=20):
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # inputs were made on the default stream
     with torch.cuda.stream(s):
         fn()
         torch.cuda.synchronize()

@@ -14,6 +14,7 @@ SHAPES = {"qkv": (6144, 4096), "o": (4096, 4096), "gate_up": (28672, 4096), "dow
 
 def gtime(fn, reps=5):
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # inputs were made on the default stream
     with torch.cuda.stream(s):
         fn()
         torch.cuda.synchronize()

@@ -72,6 +72,15 @@ def test_workspace_left_zeroed_and_deterministic():
     _check(O1, p, tag="ws")
 
 
+def test_many_sequences_one_split_each():
+    """B x Hkv >= 2 x SMs: every (sequence, KV head) is one CTA streaming its whole context through
+    the macro-tile ring (no split merge)."""
+    p = synth.kv_decode_problem(40, 32, 8, 128, 640, [640 - 7 * (i % 13) for i in range(40)], 8, seed=6400)
+    O, ws = _run(p)
+    assert ws is None
+    _check(O, p, tag="one-split")
+
+
 def test_single_token_is_its_value_row():
     """one cached token -> O = dequant(v) rounded once."""
     p = synth.kv_decode_problem(1, 8, 8, 128, 64, [1], 8, seed=6300)
