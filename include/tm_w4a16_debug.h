@@ -25,8 +25,15 @@ tm_status tm_query_gemm_config(int M, int N, int K, int* tile_m, int* split_k, i
 /* Which kernel that configuration runs: 0 = tiled (prefill; split_k > 1 = CTAs per tile along
  * K in one cluster, chosen for 65 <= M <= 512 while tiles * split_k <= 128), 1 = persistent
  * stream-K decode, 2 = decode with split_k CTAs per tile reduced in distributed shared memory
- * over a thread-block cluster (split_k = 1: one CTA per tile).                               */
+ * over a thread-block cluster (split_k = 1: one CTA per tile), 3 = register-fed decode
+ * (M <= 16; split_k CTAs per tile reduced through the workspace in CTA order).              */
 tm_status tm_query_gemm_kind(int M, int N, int K, int* kind);
+
+/* Decode kernel for M <= 16: path 0 = automatic (the TMEM decode kernel, kinds 1/2), 1 = the
+ * TMEM decode kernel, 2 = the register-fed kernel (kind 3, gemm_rf.cuh).  split in 1..8 forces the
+ * register-fed kernel's cluster mode with that many CTAs per tile (capped at the tile's 256-k
+ * chunks), split < 0 its stream-K mode with -split CTAs, 0 = automatic.                     */
+tm_status tm_set_decode_path(int path, int split);
 
 /* Decode cluster mode: 0 automatic (default), 1 never (always stream-K), 2..8 force that many
  * CTAs per tile (capped by shared memory and K), -1 one CTA per tile without a split.        */

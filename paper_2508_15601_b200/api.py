@@ -68,6 +68,7 @@ _SIGS = {
     "tm_query_gemm_config": (_I, [_I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "tm_query_gemm_kind": (_I, [_I, _I, _I, ctypes.POINTER(_I)]),
     "tm_set_decode_cluster": (_I, [_I]),
+    "tm_set_decode_path": (_I, [_I, _I]),
     "tm_set_trace": (_I, [_P, ctypes.c_int64]),
     "tm_status_string": (ctypes.c_char_p, [_I]),
     "tm_version": (ctypes.c_char_p, []),
@@ -361,6 +362,13 @@ def query_gemm_config(M, N, K):
 def set_decode_cluster(cs=0):
     """Tests/benchmarks: 0 automatic, 1 never (stream-K), 2..8 forced CTAs per tile."""
     _check(lib().tm_set_decode_cluster(cs))
+
+
+def set_decode_path(path=0, split=0):
+    """Tests/benchmarks: decode kernel for M <= 16 -- 0 automatic (the TMEM kernel), 1 the TMEM
+    decode kernel, 2 register-fed; split in 1..8 forces the register-fed kernel's cluster split,
+    split < 0 its stream-K CTA count."""
+    _check(lib().tm_set_decode_path(path, split))
 
 
 def set_trace(buf=None):

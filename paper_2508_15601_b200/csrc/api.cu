@@ -16,6 +16,7 @@
 #include "aux_kernels.cuh"
 #include "gemm_w4a16.cuh"
 #include "gemm_dec.cuh"
+#include "gemm_rf.cuh"
 #include "attn_dec.cuh"
 
 namespace {
@@ -27,6 +28,8 @@ constexpr int kNumSMsDefault = 148;
 std::atomic<int> g_override_tile{0};
 std::atomic<int> g_override_split{0};
 std::atomic<int> g_dec_cluster{0};
+std::atomic<int> g_dec_path{0};   // 0 automatic (the TMEM decode kernel), 1 TMEM decode kernel, 2 register-fed
+std::atomic<int> g_rf_split{0};   // register-fed kernel: CTAs per tile (0 = automatic)
  // 0 automatic, 1 never (stream-K), 2..8 forced size,
                                      // -1 one CTA per tile (no split)
 uint32_t* g_trace = nullptr;  // debug timeline buffer (tm_set_trace)
@@ -342,7 +345,8 @@ tm_status get_workspace(cudaStream_t stream, void* user, int64_t user_bytes, int
 
 // ---------------------------------------------------------------- launch configuration
 struct Config {
-  int kind;  // 0 = classic tiles (+ cluster split-K), 1 = persistent stream-K, 2 = decode kernel
+  int kind;  // 0 = classic tiles (+ cluster split-K), 1 = persistent stream-K, 3 = register-fed
+             // decode kernel (split = CTAs per tile), 2 = decode kernel
              // with CS CTAs per tile reduced over a thread-block cluster (split = CS)
   int NT;
   int split;  // classic: CTAs per tile along K; stream-K: number of persistent CTAs
@@ -471,7 +475,87 @@ Config decode_config(int nt, int tiles, int K) {
   return c;
 }
 
+// clusters of `cs` register-fed CTAs that fit the GPU at once (cudaOccupancyMaxActiveClusters;
+// per device, per cluster size; the NT = 16 / g = 64 instantiation has the largest footprint)
+int rf_active_clusters(int cs) {
+  static std::atomic<int> cache[kMaxDevices][9] = {};
+  const int dev = current_device();
+  if (cs < 1 || cs > 8) return 0;
+  int v = cache[dev][cs].load();
+  if (v > 0) return v;
+  auto kern = w4a16_rf_kernel<16, 64, true, OUT_ACT>;
+  static std::atomic<int> configured[kMaxDevices] = {};
+  const bool smem_ok = ensure_smem(kern, RfCfg<16, 64>::SMEM, configured) == TM_OK;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cs * 64, 1, 1);
+  cfg.blockDim = dim3(RfCfg<16, 64>::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = RfCfg<16, 64>::SMEM;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (!smem_ok || cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+    (void)cudaGetLastError();
+    n = (2 * num_sms()) / cs;  // (no device: the CPU-side query of the config)
+  }
+  cache[dev][cs].store(n);
+  return n;
+}
+
+// Register-fed decode kernel (gemm_rf.cuh), M <= 16, in one wave at two CTAs per SM (the
+// kernel's footprint allows two; under PDL the next launch's CTAs fill the SMs this launch leaves):
+//  * few tiles (tiles <= SMs): S CTAs per tile in one cluster, DSMEM reduction -- the largest
+//    S <= 8 with tiles x S <= 2 x SMs, >= 2 chunks of 256 k per CTA and all clusters resident;
+//  * many tiles: stream-K over tiles x chunks with P = 2 x SMs CTAs (every SM equally loaded: the
+//    register-fed inner loop runs at ~1.2x an SM's share of HBM, so imbalance costs directly),
+//    partial tiles added in CTA order by the last contributor.
+// Config: split = S (cluster) or -P (stream-K); debug override g_rf_split (> 0: S, < 0: -P).
+Config rf_config(int M, int N, int K) {
+  Config c{};
+  c.kind = 3;
+  c.NT = M <= 8 ? 8 : 16;
+  const int tiles = N / 128;
+  const int kc = (K + 255) / 256;
+  const long long T = static_cast<long long>(tiles) * kc;
+  int S = g_rf_split.load();
+  if (S == 0) {
+    if (tiles <= num_sms()) {
+      S = 1;
+      for (int s = 8; s >= 2; --s)
+        if (tiles * s <= 2 * num_sms() && kc >= 2 * s && tiles <= rf_active_clusters(s)) {
+          S = s;
+          break;
+        }
+    } else {
+      S = -2 * num_sms();
+    }
+  }
+  if (S > 0) {
+    if (S > 8) S = 8;
+    if (S > kc) S = kc;
+    c.split = S;
+    c.grid_x = tiles * S;
+  } else {
+    long long P = -static_cast<long long>(S);
+    if (P > T) P = T;
+    c.split = -static_cast<int>(P);
+    c.grid_x = static_cast<int>(P);
+  }
+  c.grid_y = 1;
+  return c;
+}
+
+// The register-fed kernel is opt-in (tm_set_decode_path(2, ...)): measured on the CFG#1 decode
+// shapes (scripts/rf_perf.py) it ties the TMEM kernel at M <= 8 on o/qkv and is
+// slower on gate_up/down and at M = 16, so automatic dispatch keeps the TMEM kernel.
+bool use_rf(int M) { return M <= 16 && g_dec_path.load() == 2; }
+
 Config choose_config(int M, int N, int K) {
+  if (use_rf(M)) return rf_config(M, N, K);
   Config c{};
   int nt = 16;
   const int ot = g_override_tile.load();
@@ -717,6 +801,76 @@ tm_status launch_gemm(const CUtensorMap& map, const GemmArgs& args, const Config
   }
 }
 
+template <int NT, int GROUP, bool BF16, int OUT>
+tm_status launch_rf_t(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream, UserWs ws) {
+  using Cfg = RfCfg<NT, GROUP>;
+  auto kern = w4a16_rf_kernel<NT, GROUP, BF16, OUT>;
+  static std::atomic<int> configured[kMaxDevices] = {};
+  tm_status st = ensure_smem(kern, Cfg::SMEM, configured);
+  if (st != TM_OK) return st;
+  CUtensorMap ma, ms, mz;
+  st = act_tensor_map_3d(A, g.M, g.a_ks * 64, NT, 4, BF16, &ma);
+  if (st != TM_OK) return st;
+  st = sz_tensor_map(g.scales, g.K / GROUP, g.N, &ms, Cfg::U);
+  if (st != TM_OK) return st;
+  st = sz_tensor_map(g.zeros, g.K / GROUP, g.N, &mz, Cfg::U);
+  if (st != TM_OK) return st;
+  RfArgs a;
+  a.packed = g.packed;
+  a.out = g.out;
+  a.M = g.M;
+  a.N = g.N;
+  a.K = g.K;
+  a.kc = (g.K + 255) / 256;
+  const long long T = static_cast<long long>(g.N / 128) * a.kc;
+  if (T * c.grid_x >= (1ll << 32)) return TM_ERR_UNSUPPORTED_SHAPE;  // 32-bit range math
+  a.total = static_cast<uint32_t>(T);
+  a.split = c.split > 0 ? c.split : 0;
+  a.a_ks = g.a_ks;
+  a.trace = g_trace;
+  a.partials = nullptr;
+  if (c.split <= 0) {  // stream-K: one partial tile per CTA
+    int* flags = nullptr;
+    st = get_workspace(stream, ws.ptr, ws.bytes, c.grid_x, NT, &flags, &a.partials);
+    if (st != TM_OK) return st;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(c.grid_x, 1, 1);
+  cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[2];
+  cfg.attrs = attrs;
+  cfg.numAttrs = 0;
+  static const bool no_pdl = std::getenv("TM_NO_PDL") != nullptr;  // experiments only
+  if (!no_pdl) {
+    attrs[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+    ++cfg.numAttrs;
+  }
+  if (c.split > 1) {
+    attrs[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
+    attrs[cfg.numAttrs].val.clusterDim.x = c.split;
+    attrs[cfg.numAttrs].val.clusterDim.y = 1;
+    attrs[cfg.numAttrs].val.clusterDim.z = 1;
+    ++cfg.numAttrs;
+  }
+  if (cudaLaunchKernelEx(&cfg, kern, ma, ms, mz, a) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return TM_ERR_CUDA;
+  }
+  return TM_OK;
+}
+
+template <bool BF16, int OUT>
+tm_status launch_rf(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream, UserWs ws) {
+  if (c.NT == 8)
+    return g.group == 64 ? launch_rf_t<8, 64, BF16, OUT>(A, g, c, stream, ws)
+                         : launch_rf_t<8, 128, BF16, OUT>(A, g, c, stream, ws);
+  return g.group == 64 ? launch_rf_t<16, 64, BF16, OUT>(A, g, c, stream, ws)
+                       : launch_rf_t<16, 128, BF16, OUT>(A, g, c, stream, ws);
+}
+
 // a_K: columns of A (= K, or K / 2 for W8 bit planes: the low planes reuse the activations)
 tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* scales, const void* zeros, void* C,
                       int M, int N, int K, void* stream, bool bf16, int out_kind, UserWs ws = UserWs{nullptr, 0},
@@ -759,6 +913,10 @@ tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* sca
   }
   args.trace = g_trace;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c.kind == 3) {
+    if (out_kind == OUT_F32) return launch_rf<true, OUT_F32>(A, args, c, s, ws);
+    return bf16 ? launch_rf<true, OUT_ACT>(A, args, c, s, ws) : launch_rf<false, OUT_ACT>(A, args, c, s, ws);
+  }
   if (c.kind == 1 || c.kind == 2) {
     if (out_kind == OUT_F32) return launch_sk<true, OUT_F32>(A, args, c, s, ws);
     return bf16 ? launch_sk<true, OUT_ACT>(A, args, c, s, ws) : launch_sk<false, OUT_ACT>(A, args, c, s, ws);
@@ -1014,6 +1172,10 @@ int64_t tm_gemm_workspace_bytes(int M, int N, int K, int group) {
   if (st != TM_OK) return st;
   if (M == 0) return 0;
   const Config c = choose_config(M, N, K);
+  if (c.kind == 3) {  // register-fed decode: stream-K mode needs [P][2] partial tiles + tile counters
+    if (c.split > 0) return 0;
+    return static_cast<int64_t>(ws_flag_bytes(c.grid_x) + static_cast<size_t>(c.grid_x) * c.NT * 128 * sizeof(float));
+  }
   if (c.kind != 1) return 0;
   return static_cast<int64_t>(ws_flag_bytes(c.split) + static_cast<size_t>(c.split) * c.NT * 128 * sizeof(float));
 }
@@ -1163,6 +1325,13 @@ tm_status tm_query_gemm_config(int M, int N, int K, int* tile_m, int* split_k, i
 tm_status tm_query_gemm_kind(int M, int N, int K, int* kind) {
   if (M <= 0 || N <= 0 || K <= 0 || N % 128 || K % 64 || !kind) return TM_ERR_INVALID_ARG;
   *kind = choose_config(M, N, K).kind;
+  return TM_OK;
+}
+
+tm_status tm_set_decode_path(int path, int split) {
+  if (path < 0 || path > 2 || split > 8 || split < -4096) return TM_ERR_INVALID_ARG;
+  g_dec_path.store(path);
+  g_rf_split.store(split);
   return TM_OK;
 }
 

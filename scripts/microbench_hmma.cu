@@ -130,8 +130,9 @@ void run(int warps) {
 int main() {
   for (int w : {4, 8, 16}) run<0, 4, 8>(w);
   for (int w : {4, 8, 16}) run<0, 8, 16>(w);
-  for (int w : {4, 8, 16, 32}) run<1, 4, 8>(w);
-  for (int w : {4, 8, 16, 32}) run<1, 4, 16>(w);
-  for (int w : {4, 8, 16, 32}) run<2, 4, 16>(w);
+  for (int w : {4, 8, 12, 16, 24, 32}) run<1, 4, 8>(w);
+  for (int w : {4, 8, 12, 16, 24, 32}) run<2, 4, 8>(w);
+  for (int w : {4, 8, 12, 16, 24, 32}) run<1, 4, 16>(w);
+  for (int w : {4, 8, 12, 16, 24, 32}) run<2, 4, 16>(w);
   return 0;
 }
