@@ -172,9 +172,11 @@ def make_io(layers, ms, device, nsets=2):
     return sets
 
 
-def run_step(layers, io, ms, part="all"):
+def run_step(layers, io, ms, part="all", reducer=None):
     """One step: every (M, layer, shape) GEMM.  part: "all"; "gemm" (the local GEMMs and the
-    finalize of row-parallel layers, no collective); "comm" (only the all-reduces)."""
+    finalize of row-parallel layers, no collective); "comm" (only the all-reduces).
+    reducer (--tp-reduce symm): row-parallel layers use the fused NEXT-1 epilogue (partial
+    into symmetric memory + tm_tp_allreduce_finalize) instead of NCCL + tm_tp_finalize."""
     from paper_2508_15601_b200 import api
     from paper_2508_15601_b200.tp import allreduce_sum_fp32
     n = 0
@@ -182,7 +184,14 @@ def run_step(layers, io, ms, part="all"):
         for lay in layers:
             for name, N, K in SHAPES:
                 w, b = lay[name], io[(M, name)]
-                if hasattr(w, "local_partial"):  # row-parallel: fp32 partial, all-reduce, finalize
+                if hasattr(w, "local_partial") and reducer is not None:
+                    if part != "comm":
+                        w.local_partial(b["A"], out=reducer.partial(M, N))
+                        n += 1
+                    if part != "gemm":
+                        reducer.finalize(M, N, b["C"])
+                        n += 1
+                elif hasattr(w, "local_partial"):  # row-parallel: fp32 partial, all-reduce, finalize
                     if part != "comm":
                         w.local_partial(b["A"], out=b["P"])
                         n += 1
@@ -459,6 +468,10 @@ def bench_ours(args):
     ms = [int(x) for x in args.ms.split(",")]
     L = args.layers
     layers = build_layers(L, world, rank, device)
+    reducer = None
+    if world > 1 and args.tp_reduce == "symm":
+        from paper_2508_15601_b200.tp import SymmReducer
+        reducer = SymmReducer(max(ms) * max(N for _, N, _ in SHAPES), device=device)
     sets = make_io(layers, ms, device)
     io = sets[0]["io"]
     host_A = sets[0]["A_all"].cpu().pin_memory()
@@ -467,10 +480,10 @@ def bench_ours(args):
     torch.cuda.synchronize()
     with torch.cuda.stream(stream):
         for _ in range(max(args.warmup, 3)):
-            n_launch = run_step(layers, io, ms)
+            n_launch = run_step(layers, io, ms, reducer=reducer)
     torch.cuda.synchronize()
     # the whole step -- GEMMs and, under TP, the NCCL all-reduces -- is one CUDA graph
-    graphs = [capture(lambda st=st: run_step(layers, st["io"], ms), stream) for st in sets]
+    graphs = [capture(lambda st=st: run_step(layers, st["io"], ms, reducer=reducer), stream) for st in sets]
     g = graphs[0]
     time_graph(g, 2, stream)
     nbytes, nflops = step_bytes(ms, L)
@@ -483,8 +496,8 @@ def bench_ours(args):
     te = time_e2e(graphs, sets, host_A, host_C, args.steps, stream)
     tp_detail = None
     if world > 1:
-        gg = capture(lambda: run_step(layers, io, ms, part="gemm"), stream)
-        gc = capture(lambda: run_step(layers, io, ms, part="comm"), stream)
+        gg = capture(lambda: run_step(layers, io, ms, part="gemm", reducer=reducer), stream)
+        gc = capture(lambda: run_step(layers, io, ms, part="comm", reducer=reducer), stream)
         dist.barrier()
         t_gemm = time_graph(gg, args.steps, stream)
         dist.barrier()
@@ -496,8 +509,10 @@ def bench_ours(args):
         tp_detail = dict(
             gemm_ms_per_step=round(t_gemm / args.steps * 1e3, 4), allreduce_ms_per_step=round(t_comm / args.steps * 1e3, 4),
             allreduce_bytes_per_step=int(ar_bytes), allreduces_per_step=len(ms) * L * len(ROW_PARALLEL),
-            note="max over ranks of CUDA-graph replays of (a) only the local GEMMs + finalize and (b) only the "
-                 "fp32 NCCL all-reduces; the step graph (value) runs both in order")
+            reduce=args.tp_reduce,
+            note="max over ranks of CUDA-graph replays of (a) only the local GEMMs (+ finalize for nccl) and (b) only "
+                 "the reductions (fp32 NCCL all-reduces, or the fused symmetric-memory all-reduce + finalize kernel "
+                 "for symm); the step graph (value) runs both in order")
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -628,6 +643,9 @@ def main():
     ap.add_argument("--ms", default="1,8,16")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true", help="skip the secondary M=8192 tensor-bound leg")
+    ap.add_argument("--tp-reduce", default="nccl", choices=["nccl", "symm"],
+                    help="row-parallel reduction at --gpus > 1: NCCL fp32 all-reduce + finalize, or the fused "
+                         "symmetric-memory kernel (tm_tp_allreduce_finalize, NEXT-1)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

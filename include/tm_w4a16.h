@@ -216,6 +216,27 @@ tm_status tm_attn_decode_kv8(const void* Q, const void* k_codes, const void* v_c
 /* out_bf16[i] = RNE_bf16(in_f32[i]) for i < count (TP epilogue after the all-reduce). */
 tm_status tm_tp_finalize(const float* in_f32, void* out_bf16, int64_t count, void* stream);
 
+/* Fused row-parallel epilogue over symmetric memory (§8(f) NEXT-1):
+ * replaces the fp32 all-reduce + tm_tp_finalize pair with one kernel.
+ *   out_bf16[i] = RNE_bf16( sum_{r < world} partials[r][i] ),  i < count
+ *   partials : host array of `world` device pointers -- rank r's fp32 partial [count] as mapped
+ *              in THIS process (a symmetric buffer: entry `rank` is local, the others are peer
+ *              memory reachable over NVLink; 16-byte aligned).  Written by each rank's
+ *              tm_gemm_w4a16_partial_f32 earlier on its stream.
+ *   signals  : host array of `world` device pointers -- rank r's signal pad (uint32 words,
+ *              >= TM_TP_SIGNAL_WORDS * world, zero-filled once; used exclusively by this call
+ *              while it runs).
+ *   multicast: NVLS multicast address of the partial buffers (the switch adds the ranks'
+ *              words, multimem.ld_reduce), or NULL: the sum runs over partials[] in rank order
+ *              (deterministic, bit-identical on every rank).
+ * Every rank of the group must make the matching call (the kernel contains two barriers over
+ * the signal pads: entry -- all partials complete; exit -- no rank reuses its partial buffer
+ * before every peer has read it).  world in 1..8.  Errors: TM_ERR_INVALID_ARG, TM_ERR_MISALIGNED. */
+#define TM_TP_SIGNAL_WORDS 64
+tm_status tm_tp_allreduce_finalize(const float* const* partials, uint32_t* const* signals,
+                                   const float* multicast, int rank, int world, int64_t count,
+                                   void* out_bf16, void* stream);
+
 /* Test / debug entry points ---------------------------------------------------------
  * tm_unpack_w4  : packed -> uint8 [K][N] codes 0..15 (inverse of tm_pack_w4, bit-exact).
  * tm_dequant_w4 : packed + scales + zeros -> W [K][N] in the activation dtype using the

@@ -62,6 +62,8 @@ _SIGS = {
     "tm_gemm_w4a16_grouped": (_I, [_P, ctypes.POINTER(tm_packed_w4), _P, _P, _P, ctypes.POINTER(ctypes.c_int32), _I,
                                    _I, _I, _P]),
     "tm_tp_finalize": (_I, [_P, _P, ctypes.c_int64, _P]),
+    "tm_tp_allreduce_finalize": (_I, [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), _P, _I, _I,
+                                      ctypes.c_int64, _P, _P]),
     "tm_unpack_w4": (_I, [ctypes.POINTER(tm_packed_w4), _P, _P]),
     "tm_dequant_w4": (_I, [ctypes.POINTER(tm_packed_w4), _P, _P, _P, _I, _P]),
     "tm_set_gemm_override": (_I, [_I, _I]),
@@ -345,6 +347,19 @@ def debug_dequant_int(packed, zeros, dtype="bf16", stream=None):
     out = torch.empty((packed.K, packed.N), dtype=tdt, device=packed.data.device)
     _check(lib().tm_debug_dequant_int(ctypes.byref(packed.desc), _ptr(zeros), _ptr(out),
                                       0 if dtype == "bf16" else 1, _stream(stream)))
+    return out
+
+
+def tp_allreduce_finalize(partial_ptrs, signal_ptrs, multicast_ptr, rank, world, count, out, stream=None):
+    """tm_tp_allreduce_finalize: out (bf16 CUDA tensor, >= count elements) = RNE(sum over ranks
+    of the fp32 partials); pointers are this process's mappings of the symmetric buffers."""
+    _require_cuda(out)
+    P = (ctypes.c_void_p * len(partial_ptrs))(*[int(x) for x in partial_ptrs])
+    S = (ctypes.c_void_p * len(signal_ptrs))(*[int(x) for x in signal_ptrs])
+    if len(partial_ptrs) < world or len(signal_ptrs) < world:
+        raise TMError("tp_allreduce_finalize: fewer pointers than ranks")
+    _check(lib().tm_tp_allreduce_finalize(P, S, ctypes.c_void_p(int(multicast_ptr) or None), rank, world, int(count),
+                                          _ptr(out), _stream(stream)))
     return out
 
 

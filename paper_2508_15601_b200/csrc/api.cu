@@ -18,6 +18,7 @@
 #include "gemm_dec.cuh"
 #include "gemm_rf.cuh"
 #include "attn_dec.cuh"
+#include "tp_reduce.cuh"
 
 namespace {
 
@@ -1298,6 +1299,28 @@ tm_status tm_tp_finalize(const float* in_f32, void* out_bf16, int64_t count, voi
   const long long tail = count - n4 * 4;
   if (tail > 0)
     tp_finalize_tail_kernel<<<1, 32, 0, s>>>(in_f32, static_cast<__nv_bfloat16*>(out_bf16), n4 * 4, count);
+  return from_cuda(cudaGetLastError());
+}
+
+tm_status tm_tp_allreduce_finalize(const float* const* partials, uint32_t* const* signals, const float* multicast,
+                                   int rank, int world, int64_t count, void* out_bf16, void* stream) {
+  if (!partials || !signals || !out_bf16 || count < 0) return TM_ERR_INVALID_ARG;
+  if (world < 1 || world > kTpMaxRanks || rank < 0 || rank >= world) return TM_ERR_INVALID_ARG;
+  TpReduceArgs a{};
+  for (int r = 0; r < world; ++r) {
+    if (!partials[r] || !signals[r]) return TM_ERR_INVALID_ARG;
+    if (!aligned16(partials[r]) || (reinterpret_cast<uintptr_t>(signals[r]) & 3)) return TM_ERR_MISALIGNED;
+    a.partials[r] = partials[r];
+    a.signals[r] = signals[r];
+  }
+  if (!aligned16(out_bf16) || (multicast && !aligned16(multicast))) return TM_ERR_MISALIGNED;
+  a.multicast = multicast;
+  a.out = static_cast<__nv_bfloat16*>(out_bf16);
+  a.count = count;
+  a.rank = rank;
+  a.world = world;
+  // every rank runs the barriers, also for count == 0 (peers may have work)
+  tp_allreduce_finalize_kernel<<<kTpBlocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
   return from_cuda(cudaGetLastError());
 }
 

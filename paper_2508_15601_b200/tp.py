@@ -9,6 +9,12 @@ NVLink on the GPU box, reading R13), and tm_tp_finalize rounds once to bf16.
 
 The shard arithmetic here is plain index math (host side); the GEMM/finalize run in the
 library.  `shard_bounds` is also what the CPU gloo tests check against the oracle.
+
+SymmReducer (§8(f) NEXT-1) replaces the all-reduce + finalize pair with the library's fused
+kernel over torch symmetric memory: each rank's GEMM writes its fp32 partial straight into a
+symmetric buffer, tm_tp_allreduce_finalize adds the ranks' partials (NVLS multimem.ld_reduce
+through the multicast address when the fabric provides one, else a rank-ordered sum over the
+peers' NVLink mappings) and rounds once to bf16 -- one launch of ours instead of NCCL + one.
 """
 
 import torch
@@ -48,6 +54,29 @@ class ColumnParallelW4:
         return api.gemm_w4a16(A, self.packed, self.s, self.z, out=out)
 
 
+class SymmReducer:
+    """Fused TP all-reduce + finalize over a torch symmetric-memory fp32 buffer of max_elems."""
+
+    def __init__(self, max_elems, group=None, device=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        group = group or dist.group.WORLD
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.buf = symm_mem.empty(max_elems, dtype=torch.float32, device=device or torch.cuda.current_device())
+        self.handle = symm_mem.rendezvous(self.buf, group.group_name)
+        self.partial_ptrs = list(self.handle.buffer_ptrs)
+        self.signal_ptrs = list(self.handle.signal_pad_ptrs)
+        self.multicast_ptr = int(self.handle.multicast_ptr or 0)
+
+    def partial(self, M, N):
+        """This rank's fp32 partial [M][N] (the head of the symmetric buffer)."""
+        return self.buf[:M * N].view(M, N)
+
+    def finalize(self, M, N, out, stream=None):
+        from . import api
+        return api.tp_allreduce_finalize(self.partial_ptrs, self.signal_ptrs, self.multicast_ptr, self.rank,
+                                         self.world, M * N, out, stream=stream)
+
+
 class RowParallelW4:
     """K-sharded W4A16 layer: fp32 partial + all-reduce + finalize.  When K is not divisible into
     `world` shards of whole groups (Qwen2-72B down: K = 29568 = 231 groups of 128), K is padded to
@@ -80,11 +109,18 @@ class RowParallelW4:
             A = torch.nn.functional.pad(A, (0, self.Kp - self.K))
         return A[:, self.lo:self.hi].contiguous()
 
-    def __call__(self, A, partial=None, out=None):
+    def __call__(self, A, partial=None, out=None, reducer=None):
         """A: full activations [M][K] (replicated) or this rank's shard [M][hi - lo]; returns
-        bf16 C [M][N] on every rank."""
+        bf16 C [M][N] on every rank (reducer: a SymmReducer -> the fused NEXT-1 epilogue)."""
         from . import api
-        part = self.local_partial(self.shard_input(A) if A.shape[1] == self.K else A, out=partial)
+        A_loc = self.shard_input(A) if A.shape[1] == self.K else A
+        if reducer is not None:
+            M = A_loc.shape[0]
+            if out is None:
+                out = torch.empty(M, self.N, dtype=torch.bfloat16, device=A_loc.device)
+            self.local_partial(A_loc, out=reducer.partial(M, self.N))
+            return reducer.finalize(M, self.N, out)
+        part = self.local_partial(A_loc, out=partial)
         if dist.is_initialized() and dist.get_world_size(self.pg) > 1:
             dist.all_reduce(part, op=dist.ReduceOp.SUM, group=self.pg)
         return api.tp_finalize(part, out=out)
