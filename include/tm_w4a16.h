@@ -166,7 +166,9 @@ int64_t tm_gemm_workspace_bytes(int M, int N, int K, int group);
  *   a_dtype   : TM_DTYPE_BF16 or TM_DTYPE_FP16 (A)
  *   c_dtype   : a_dtype (rounded output) or TM_DTYPE_F32 (fp32 partial, bf16 A only)
  *   workspace : device buffer of >= tm_gemm_workspace_bytes(M, N, K, group) bytes, 16-byte
- *               aligned, ZERO-FILLED once before its first use (every call leaves it zeroed);
+ *               aligned, ZERO-FILLED once before its first use; a buffer used by the
+ *               register-fed decode path (tm_set_decode_path(2, ...)) must not be shared with
+ *               calls that run the other kernels (its partial words must stay zero between launches);
  *               may be NULL (with workspace_bytes 0) when that size is 0.  One workspace
  *               must not be used by two calls that can run concurrently.
  * Errors: TM_ERR_INVALID_ARG for a missing/too small workspace or a dtype pair not listed. */

@@ -39,9 +39,10 @@ tm_status tm_set_decode_path(int path, int split);
  * CTAs per tile (capped by shared memory and K), -1 one CTA per tile without a split.        */
 tm_status tm_set_decode_cluster(int cs);
 
-/* Debug timeline: when buf != NULL every GEMM CTA writes 160 uint32 events (clock cycles
- * since CTA start; slot 0 = %globaltimer ns) at buf[cta * 160 + slot] (TM_PROFILE builds).
- * NULL disables tracing (the default).                                                       */
+/* Debug timeline: when buf != NULL the CTAs of the tiled (prefill) kernel write 160 uint32
+ * events at buf[cta * 160 + slot] (slot 0 = %globaltimer ns at start, others clock cycles
+ * since start) and those of the register-fed decode kernel 64 %globaltimer (ns) events at
+ * buf[cta * 64 + slot].  NULL disables tracing (the default).                               */
 tm_status tm_set_trace(void* buf, int64_t bytes);
 
 /* The decode kernel's MMA operand for every weight (reading R6b), through the kernel's own

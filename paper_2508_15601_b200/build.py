@@ -30,7 +30,7 @@ def _inputs():
 
 
 def up_to_date():
-    if not os.path.exists(LIB) or os.environ.get("TM_PROFILE") == "1" or os.environ.get("TM_DIAG") or os.environ.get("TM_DEFS"):
+    if not os.path.exists(LIB) or os.environ.get("TM_DEFS"):
         return False
     t = os.path.getmtime(LIB)
     return all(os.path.getmtime(f) <= t for f in _inputs())
@@ -39,10 +39,7 @@ def up_to_date():
 def build(force=False, verbose=False):
     if not force and up_to_date():
         return LIB
-    extra = ["-DTM_PROFILE=1"] if os.environ.get("TM_PROFILE") == "1" else []
-    if os.environ.get("TM_DIAG"):
-        extra.append("-DTM_DIAG=" + os.environ["TM_DIAG"])
-    extra += ["-D" + d for d in os.environ.get("TM_DEFS", "").split()]  # A/B experiments only
+    extra = ["-D" + d for d in os.environ.get("TM_DEFS", "").split()]  # A/B experiments only
     cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
            *[os.path.join(CSRC, s) for s in SOURCES]]
     res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)

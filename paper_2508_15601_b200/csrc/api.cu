@@ -289,17 +289,19 @@ struct Workspace {
 struct WsKey {
   int dev;
   cudaStream_t stream;
-  bool operator==(const WsKey& o) const { return dev == o.dev && stream == o.stream; }
+  int kind;  // 0: TMEM decode kernels (flags zero between launches), 1: register-fed kernel
+             // (self-validating partial words, all zero between launches: never shared)
+  bool operator==(const WsKey& o) const { return dev == o.dev && stream == o.stream && kind == o.kind; }
 };
 struct WsKeyHash {
-  size_t operator()(const WsKey& k) const { return reinterpret_cast<size_t>(k.stream) * 31u + k.dev; }
+  size_t operator()(const WsKey& k) const { return reinterpret_cast<size_t>(k.stream) * 31u + k.dev * 7u + k.kind; }
 };
 std::mutex g_ws_mu;
 std::unordered_map<WsKey, Workspace, WsKeyHash> g_ws;
 
-tm_status library_workspace(cudaStream_t stream, size_t need, void** out) {
+tm_status library_workspace(cudaStream_t stream, size_t need, void** out, int kind = 0) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  Workspace& w = g_ws[WsKey{current_device(), stream}];
+  Workspace& w = g_ws[WsKey{current_device(), stream, kind}];
   if (w.bytes < need) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
@@ -328,7 +330,7 @@ tm_status library_workspace(cudaStream_t stream, size_t need, void** out) {
 
 // flags + partials for `ctas` CTAs of NT-token tiles, from the caller's buffer or the library's
 tm_status get_workspace(cudaStream_t stream, void* user, int64_t user_bytes, int ctas, int nt, int** flags,
-                        float** partials) {
+                        float** partials, int kind = 0) {
   const size_t fb = ws_flag_bytes(ctas);
   const size_t need = fb + static_cast<size_t>(ctas) * nt * 128 * sizeof(float);
   void* base = user;
@@ -336,7 +338,7 @@ tm_status get_workspace(cudaStream_t stream, void* user, int64_t user_bytes, int
     if (user_bytes < static_cast<int64_t>(need)) return TM_ERR_INVALID_ARG;
     if (!aligned16(user)) return TM_ERR_MISALIGNED;
   } else {
-    tm_status st = library_workspace(stream, need, &base);
+    tm_status st = library_workspace(stream, need, &base, kind);
     if (st != TM_OK) return st;
   }
   *flags = static_cast<int*>(base);
@@ -832,7 +834,7 @@ tm_status launch_rf_t(const void* A, const GemmArgs& g, const Config& c, cudaStr
   a.partials = nullptr;
   if (c.split <= 0) {  // stream-K: one partial tile per CTA
     int* flags = nullptr;
-    st = get_workspace(stream, ws.ptr, ws.bytes, c.grid_x, NT, &flags, &a.partials);
+    st = get_workspace(stream, ws.ptr, ws.bytes, c.grid_x, NT, &flags, &a.partials, 1);
     if (st != TM_OK) return st;
   }
   cudaLaunchConfig_t cfg{};

@@ -239,37 +239,6 @@ struct RingPos {
   }
 };
 
-#ifndef TM_PROFILE
-#define TM_PROFILE 0
-#endif
-// diagnostics only (wrong results): bit 0 no weight loads, bit 1 no dequant math, bit 2 no MMAs,
-// bit 3 no activation loads, bit 4 no tcgen05.st of operands, bit 5 no tcgen05.ld of D,
-// bit 6 tcgen05.st of half the blobs, bit 7 half the MMAs, bit 8 one MMA issuer, bit 9 MMA issuer
-// waits for its chunk's completion, bit 10 MMA issuer skips its waits, bit 11 no fence before the MMAs,
-// bit 12 MMA issuer alone, bit 13 dequant/scale warps skip their tcgen05 fences,
-// bit 14 no scale warps, bit 15 no weight producer / dequant warps
-#ifndef TM_DIAG
-#define TM_DIAG 0
-#endif
-#if TM_PROFILE
-// per-thread accumulators in registers, flushed once at kernel end (a global read-modify-write
-// per event would put its own latency inside the measured intervals)
-#define DCLK() clock64()
-#define DACC(slot, v) (prof[(slot) - 136] += static_cast<uint32_t>(v))
-// timeline marks: cycles since CTA start (slot 0 = %globaltimer low bits at CTA start)
-#define DMARK(slot)                                                                             \
-  do {                                                                                          \
-    if (args.trace) args.trace[blockIdx.x * 160 + (slot)] = static_cast<uint32_t>(clock64() - t_start); \
-  } while (0)
-#else
-#define DMARK(slot) \
-  do {              \
-  } while (0)
-#define DCLK() 0ll
-#define DACC(slot, v) \
-  do {                \
-  } while (0)
-#endif
 
 // Iterate the CTA's segments: a segment is the part of one (m-tile, n-tile) inside [u0, u1).
 #define DEC_FOR_SEGMENTS                                                                            \
@@ -311,29 +280,7 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);  // warp-uniform
   const uint32_t lane = threadIdx.x & 31;
-#if TM_PROFILE
-  uint32_t prof[24] = {};
-  const long long t_start = clock64();
-  if (args.trace && threadIdx.x == 0) {
-    uint64_t gt;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    args.trace[blockIdx.x * 160] = static_cast<uint32_t>(gt);
-    uint32_t smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    args.trace[blockIdx.x * 160 + 11] = smid;
-  }
-#endif
 
-#if TM_PROFILE
-  if (TM_DIAG & 131072) {  // diagnostic: an empty CTA (trace start/end only)
-    if (args.trace && threadIdx.x == 0) {
-      uint64_t gt;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-      args.trace[blockIdx.x * 160 + 6] = static_cast<uint32_t>(gt);
-    }
-    return;
-  }
-#endif
   const int P = gridDim.x;
   const int p = blockIdx.x;
   const uint32_t T = static_cast<uint32_t>(args.total);
@@ -363,7 +310,7 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
   const int box_mask = ((Cfg::SZG << gshift) / Cfg::CH) - 1;  // chunks per s/z box - 1 (2 or 4 chunks)
   const int DR = dec_dring<NT>(args.group);           // D ring entries (1, 2 or 4)
   const int dr_mask = DR - 1, dr_shift = DR == 4 ? 2 : DR - 1;
-  const int NISSUE = (TM_DIAG & 256) ? 1 : dec_nissue<NT>(DR);  // 1 or 2
+  const int NISSUE = dec_nissue<NT>(DR);  // 1 or 2
   const int is_mask = NISSUE - 1;
   const int DSTRIDE = (Cfg::CH >> gshift) * NT;        // D columns per ring entry
 
@@ -382,15 +329,11 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
       for (int c = c0; c < c1; ++c, ++i) {
         if (i < w_i) continue;
         if (i >= i_end) return;
-        const long long q0 = DCLK();
         mbar_wait(bar_emptyw + 8 * w_st.slot, w_st.phase ^ 1u);  // the dequant of chunk i - NW read it
-        const long long q1 = DCLK();
         const int kb0 = c * Cfg::BLOBS;
         const int nb = (KS - kb0) < Cfg::BLOBS ? (KS - kb0) : Cfg::BLOBS;
         const uint32_t fb = bar_fullw + 8 * w_st.slot;
-        if (TM_DIAG & 1) {
-          if (elect_one()) mbar_arrive(fb);
-        } else if (elect_one()) {
+        if (elect_one()) {
           mbar_arrive_expect_tx(fb, nb * 4096);
           bulk_g2s_hint(w0 + w_st.slot * Cfg::W_BYTES,
                         args.packed + (static_cast<size_t>(dt.blob0) + static_cast<size_t>(nt) * KS + kb0) * 4096,
@@ -399,16 +342,10 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
         __syncwarp();
         w_st.advance(NW);
         w_i = i + 1;
-        if (lane == 0) {
-          DACC(150, q1 - q0);
-          DACC(151, DCLK() - q1);
-          DACC(152, 1);
-        }
       }
     }
   };
   if (warp == Cfg::W_PRODW) {
-    if (lane == 0) DMARK(10);
     constexpr int NBAR = 2 * NW + 3 * NR + DR_MAX + 2 * Cfg::SZ_SLOTS;
     for (int b = static_cast<int>(lane); b < NBAR; b += 32) {
       uint32_t cnt;
@@ -425,7 +362,6 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
     if (push && lane == 0) mbar_init(bar_red, (CS - 1) * 128);
     fence_mbar_init();
     __syncwarp();
-    if (lane == 0) DMARK(7);
     if (lane == 0) {
       prefetch_tmap(&tmap_a);
       prefetch_tmap(&tmap_s);
@@ -436,10 +372,8 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
     if (TM_EARLY_W > 0) produce_w(TM_EARLY_W);
   }
   if (warp == Cfg::W_MMA) {
-    if (lane == 0) DMARK(9);
     tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
     tmem_relinquish();
-    if (lane == 0) DMARK(8);
   }
   tc_fence_before();
   __syncthreads();
@@ -449,7 +383,6 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
   if (push) cluster_arrive_relaxed();
   bool cl_waited = false;  // push mode: this thread has consumed its setup cluster arrive
   const uint32_t tmem_base = *tmem_slot_ptr;
-  if (threadIdx.x == 0) DMARK(1);
   // PDL: let the next kernel in the stream start launching now; its CTAs take SMs as ours exit,
   // and it waits (griddepcontrol.wait) before reading anything this kernel writes.
   grid_dependency_launch();
@@ -467,7 +400,6 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
     // last (end of the head holder's range), so the head holder finalises: it waits for the
     // contributors' flags (long set by then), adds their partials in fixed CTA order
     // (deterministic) and stores.  A tail only stores its partial and raises its flag.
-    const long long qe = DCLK();
     const uint32_t tile_lo = static_cast<uint32_t>(t) * kc;
     const uint32_t tile_hi = tile_lo + kc;
     const int n = nt * 128 + row;
@@ -525,44 +457,8 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
       for (int m = 0; m < NT; ++m)
         if (m < mcount) dec_store<BF16, OUT>(args.out, args.N, mb + m, n, acc[m]);
     }
-    if (et == 0) DACC(157, DCLK() - qe);
   };
-  if (TM_DIAG & 65536) {
-    // diagnostic: setup and teardown only
-  } else if (TM_DIAG & 4096) {
-    // diagnostic: MMA issuer 0 alone, back-to-back chunks with commit + wait (no other roles)
-    if (warp == Cfg::W_MMA) {
-      constexpr uint32_t idesc = umma_idesc_f16(BF16, 128, NT);
-      const long long q0 = DCLK();
-      const int nchunks = static_cast<int>(u1 - u0);
-      for (int i = 0; i < nchunks; ++i) {
-        const int r = i % NR;
-        if (elect_one()) {
-          for (int g = 0; g < 2; ++g)
-            for (int bb = 0; bb < 2; ++bb) {
-              const int blob = g * 2 + bb;
-              const uint64_t bd = umma_desc_sw128(a0 + r * Cfg::ACT_BYTES + blob * (NT * 128));
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                mma_ts(tmem_d0 + (i & 3) * 32 + g * 16, tmem_a0 + ((i % 3) * 4 + blob) * 32 + 8 * j, bd + 2 * j, idesc,
-                       (bb | j) != 0);
-            }
-          tc_commit(bar_done + 8 * r);
-        }
-        __syncwarp();
-        mbar_wait(bar_done + 8 * r, (i / NR) & 1);
-      }
-      if (lane == 0) {
-        DACC(147, DCLK() - q0);
-        DACC(140, nchunks);
-        DACC(138, 0);
-      }
-    }
-  } else if ((TM_DIAG & 32768) && (warp == Cfg::W_PRODW || warp >= Cfg::W_DEQ)) {
-    // diagnostic: no weight producer, no dequant
-  } else if ((TM_DIAG & 16384) && warp >= Cfg::W_SCALE && warp < Cfg::W_SCALE + 4) {
-    // diagnostic: no scale warps
-  } else if (warp == Cfg::W_PRODW) {
+  if (warp == Cfg::W_PRODW) {
     // ---------------------------------------------------------------- producer W (the rest)
     produce_w(1 << 30);
   } else if (warp == Cfg::W_PRODA) {
@@ -593,16 +489,12 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
           grid_dependency_wait();  // activations may come from the previous kernel
           waited_dep = true;
         }
-        const long long q0 = DCLK();
         if (i >= NR) {
-          if (!(TM_DIAG & 1024)) mbar_wait(bar_done + 8 * prev.slot, prev.phase);  // MMA of chunk i - NR read the slot
+          mbar_wait(bar_done + 8 * prev.slot, prev.phase);  // MMA of chunk i - NR read the slot
           prev.advance(NR);
         }
-        const long long q1 = DCLK();
         const uint32_t fb = bar_fulla + 8 * st.slot;
-        if (TM_DIAG & 8) {
-          if (elect_one()) mbar_arrive(fb);
-        } else if (elect_one()) {
+        if (elect_one()) {
           mbar_arrive_expect_tx(fb, Cfg::ACT_BYTES);
           // W8 bit planes: the low planes (k >= K_A) reuse the activations of the high planes
           const int akb = c * Cfg::BLOBS >= args.a_ks ? c * Cfg::BLOBS - args.a_ks : c * Cfg::BLOBS;
@@ -610,10 +502,6 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
         }
         __syncwarp();
         st.advance(NR);
-        if (lane == 0) {
-          DACC(153, q1 - q0);
-          DACC(154, DCLK() - q1);
-        }
       }
     }
   } else if (warp == Cfg::W_MMA || warp == Cfg::W_MMA + 1) {
@@ -640,17 +528,11 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
           const int nb = (KS - kb0) < Cfg::BLOBS ? (KS - kb0) : Cfg::BLOBS;
           const int ng = nb >> bshift;
           const uint32_t act = a0 + r * Cfg::ACT_BYTES;
-          const long long q0 = DCLK();
-          if (!(TM_DIAG & 1024)) {
-            mbar_wait(bar_fulla + 8 * r, rph);                    // activations in SMEM
-            if (!(TM_DIAG & 32768)) mbar_wait(bar_ready + 8 * r, rph);  // operands in TMEM
-          }
-          const long long q1 = DCLK();
+          mbar_wait(bar_fulla + 8 * r, rph);  // activations in SMEM
+          mbar_wait(bar_ready + 8 * r, rph);  // operands in TMEM
           // D slots read (FS: the set's D region is free once the set arrived ready for this chunk)
-          if (!FS && !(TM_DIAG & (1024 | 16384))) mbar_wait(bar_dfree + 8 * dr, ((i >> dr_shift) & 1) ^ 1);
-          if (!(TM_DIAG & 2048)) tc_fence_after();
-          const long long q2 = DCLK();
-          long long q3 = q2, qf = q2;
+          if (!FS) mbar_wait(bar_dfree + 8 * dr, ((i >> dr_shift) & 1) ^ 1);
+          tc_fence_after();
           if (elect_one()) {
             const uint32_t d_base = tmem_d0 + (FS ? ac : dr) * DSTRIDE;
             const uint32_t a_base = tmem_a0 + ac * Cfg::BLOBS * 32;
@@ -662,14 +544,11 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
               for (int blob = 0; blob < Cfg::BLOBS; ++blob)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                  if ((TM_DIAG & 128) && (j & 1)) continue;
                   mma_ts(d_base + (blob / BPG) * Cfg::DCOLS, a_base + blob * 32 + 8 * j,
                          bdesc + ((blob * NT * 128) >> 4) + 2 * j, idesc, ((blob % BPG) | j) != 0 ? 1u : 0u);
-                  if (TM_PROFILE && blob == 0 && j == 0) qf = DCLK();
                 }
             };
-            if (TM_DIAG & 4) {
-            } else if (nb == Cfg::BLOBS && bpg == 2) {
+            if (nb == Cfg::BLOBS && bpg == 2) {
               issue_full(std::integral_constant<int, 2>{});
             } else if (nb == Cfg::BLOBS) {
               issue_full(std::integral_constant<int, 1>{});
@@ -685,22 +564,9 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
                 }
               }
             }
-            q3 = DCLK();
             tc_commit(bar_done + 8 * r);
           }
           __syncwarp();
-          if (TM_DIAG & 512) {  // MMA completion latency (diagnostic: serialises chunks)
-            mbar_wait(bar_done + 8 * r, rph);
-            if (me == 0 && lane == 0) DACC(147, DCLK() - q2);
-          }
-          if (me == 0 && lane == 0) {
-            DACC(136, q1 - q0);
-            DACC(137, q2 - q1);
-            DACC(138, q3 - q2);
-            DACC(145, qf - q2);
-            DACC(139, DCLK() - q3);
-            DACC(140, 1);
-          }
         }
       }
     }
@@ -738,10 +604,7 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
         const int ws = wp.slot;
         const int kb0 = c * Cfg::BLOBS;
         const int nb = (KS - kb0) < Cfg::BLOBS ? (KS - kb0) : Cfg::BLOBS;
-        const long long q0 = DCLK();
         mbar_wait(bar_fullw + 8 * ws, wp.phase);  // the chunk's packed weights landed
-        const long long q1 = DCLK();
-        if (mine == 0 && warp == Cfg::W_DEQ && lane == 0) DMARK(2);
         const uint8_t* wst = w_ptr0 + ws * Cfg::W_BYTES + row * 16;
         // zero operands of the chunk's groups (g = 128: 2, g = 64: 4), before the slot wait
         const int gi0 = ((kb0 * 64) >> gshift) - g_base;
@@ -751,36 +614,25 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
         // this set's TMEM slot was last read by the MMA of chunk i - NDS (FS: waited at the end of
         // the set's previous chunk already)
         const auto wait_slot = [&]() {
-          if (!FS && mine > 0 && !(TM_DIAG & 1024)) mbar_wait(bar_done + 8 * rp_prev.slot, rp_prev.phase);
-          if (!(TM_DIAG & 8192)) tc_fence_after();
+          if (!FS && mine > 0) mbar_wait(bar_done + 8 * rp_prev.slot, rp_prev.phase);
+          tc_fence_after();
         };
-        const long long q2 = DCLK();
         // one blob: 8 LAYOUT v1 words (two LDS.128) -> 32 operand registers -> tcgen05.st x32
         const auto blob_regs = [&](int bb, uint32_t z2, uint32_t (&rr)[32]) {
           const uint4 xa = *reinterpret_cast<const uint4*>(wst + bb * 4096);
           const uint4 xb = *reinterpret_cast<const uint4*>(wst + bb * 4096 + 2048);
-          if (TM_DIAG & 2) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) rr[j] = (j & 1 ? xa.x : xb.y) + j;
-          } else {
-            deq_word_int<BF16>(xa.x, z2, rr + 0);
-            deq_word_int<BF16>(xa.y, z2, rr + 4);
-            deq_word_int<BF16>(xa.z, z2, rr + 8);
-            deq_word_int<BF16>(xa.w, z2, rr + 12);
-            deq_word_int<BF16>(xb.x, z2, rr + 16);
-            deq_word_int<BF16>(xb.y, z2, rr + 20);
-            deq_word_int<BF16>(xb.z, z2, rr + 24);
-            deq_word_int<BF16>(xb.w, z2, rr + 28);
-          }
+          deq_word_int<BF16>(xa.x, z2, rr + 0);
+          deq_word_int<BF16>(xa.y, z2, rr + 4);
+          deq_word_int<BF16>(xa.z, z2, rr + 8);
+          deq_word_int<BF16>(xa.w, z2, rr + 12);
+          deq_word_int<BF16>(xb.x, z2, rr + 16);
+          deq_word_int<BF16>(xb.y, z2, rr + 20);
+          deq_word_int<BF16>(xb.z, z2, rr + 24);
+          deq_word_int<BF16>(xb.w, z2, rr + 28);
         };
-        const auto blob_st = [&](int bb, const uint32_t (&rr)[32]) {
-          if ((TM_DIAG & 16) || ((TM_DIAG & 64) && bb >= 2))
-            keep_alive_32(rr);
-          else
-            tmem_st_32x32b_x32(a_slot + bb * 32, rr);
-        };
+        const auto blob_st = [&](int bb, const uint32_t (&rr)[32]) { tmem_st_32x32b_x32(a_slot + bb * 32, rr); };
         const auto blob_to_tmem = [&](int bb, uint32_t z2) {
-          if (TM_ST_HALF && !(TM_DIAG & (2 | 16 | 64))) {
+          if (TM_ST_HALF) {
             // two halves (16 k-pairs each): the second half's LDS + math overlaps the first store
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -813,7 +665,7 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
           if (pre) blob_regs(0, z0, r0);
           wait_slot();
           if (!pre) blob_regs(0, z0, r0);
-          if (TM_ST_HALF && !(TM_DIAG & (2 | 16 | 64))) {
+          if (TM_ST_HALF) {
             tmem_st_32x32b_x16(a_slot, r0);
             tmem_st_32x32b_x16(a_slot + 16, r0 + 16);
           } else {
@@ -833,13 +685,10 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
           for (int bb = 0; bb < nb; ++bb) blob_to_tmem(bb, zop(bb >> bshift));
         }
         rp_prev = rp;
-        const long long q3 = DCLK();
         mbar_arrive(bar_emptyw + 8 * ws);  // all LDS of the chunk's codes have completed
-        if (!(TM_DIAG & 8192)) tc_wait_st();
-        const long long q4 = DCLK();
-        if (!(TM_DIAG & 8192)) tc_fence_before();
+        tc_wait_st();
+        tc_fence_before();
         mbar_arrive(bar_ready + 8 * r);
-        if (lane == 0 && quarter == 0) DMARK(3);  // last chunk's operands written (latest wins)
         ++mine;
         if constexpr (FS) {
           // fused scale: once this chunk's MMAs completed, C += s_g * D_g for its groups (the D
@@ -881,14 +730,6 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
           }
           tc_fence_before();
         }
-        if (warp == Cfg::W_DEQ && lane == 0) {
-          DACC(143, q1 - q0);
-          DACC(144, q2 - q1);
-          DACC(146, DCLK() - q2);
-          DACC(148, 1);
-          DACC(159, q3 - q2);
-          DACC(149, q4 - q3);
-        }
       }
       if constexpr (FS) {
         // segment end (the CTA's only one: FS is cluster split-K): once every set is done with
@@ -928,24 +769,20 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
       for (int m = 0; m < NT; ++m) acc[m] = 0.f;
       int g_base = 0;
       for (int c = c0; c < c1; ++c) {
-        const long long qi = DCLK();
         if (((c - c0) & box_mask) == 0) {
           if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));
           ++box;
           mbar_wait(bar_szfull + 8 * (box % Cfg::SZ_SLOTS), (box / Cfg::SZ_SLOTS) & 1);
           g_base = (c * Cfg::CH) >> gshift;
         }
-        if (et == 0) DACC(155, DCLK() - qi);
         const uint8_t* ss = sz_ptr0 + (box % Cfg::SZ_SLOTS) * 2 * Cfg::SZ_BOX;
         const int kb0 = c * Cfg::BLOBS;
         const int nb = (KS - kb0) < Cfg::BLOBS ? (KS - kb0) : Cfg::BLOBS;
         const int ng = nb >> bshift;
         const int r = rps.slot;
         const int dr = ci & dr_mask;
-        const long long q0 = DCLK();
-        if (!(TM_DIAG & 1024)) mbar_wait(bar_done + 8 * r, rps.phase);
-        if (!(TM_DIAG & 8192)) tc_fence_after();
-        const long long q1 = DCLK();
+        mbar_wait(bar_done + 8 * r, rps.phase);
+        tc_fence_after();
         const uint32_t d_row = tmem_d0 + dr * DSTRIDE + lane_off;
         const int gi0 = ((kb0 * 64) >> gshift) - g_base;
         const auto scale_of = [&](int g) {
@@ -955,12 +792,7 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
           // whole 32-column loads (NT = 16: two groups per load), one wait per load
           for (int c0 = 0; c0 < ng * NT; c0 += 32) {
             uint32_t v[32];
-            if (TM_DIAG & 32) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = 0;
-            } else {
-              tmem_ld_32x32b_x32(d_row + c0, v);
-            }
+            tmem_ld_32x32b_x32(d_row + c0, v);
             const float s0 = scale_of(c0 / NT);
             const float s1 = NT == 16 ? scale_of(c0 / NT + 1) : s0;
             tc_wait_ld();
@@ -980,38 +812,21 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
             }
           }
         }
-        if (!(TM_DIAG & 8192)) tc_fence_before();
+        tc_fence_before();
         mbar_arrive(bar_dfree + 8 * dr);
-        if (et == 0) {
-          DACC(141, q1 - q0);
-          DACC(142, DCLK() - q1);
-          DACC(156, DCLK() - qi);
-          DACC(158, 1);
-        }
         ++ci;
         rps.advance(NR);
       }
-      if (et == 0) DMARK(4);  // accumulation of this segment finished (latest segment wins)
       seg_end(acc, t, u, cend, row, et);
     }
     if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % Cfg::SZ_SLOTS));
   }
 
-  if (warp == Cfg::W_SCALE && lane == 0) DMARK(5);  // epilogue finished
-  if (lane == 0 && warp < 20) DMARK(12 + warp);     // this warp's role finished
-#if TM_PROFILE
-  if (args.trace) {
-    for (int k = 0; k < 24; ++k)
-      if (prof[k]) atomicAdd(args.trace + blockIdx.x * 160 + 136 + k, prof[k]);
-  }
-#endif
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) DMARK(32);  // every role finished
   if (warp == Cfg::W_MMA) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
-    if (lane == 0) DMARK(33);
   }
   if (push) {
     if (!cl_waited) cluster_wait();  // pairs the setup arrive (threads outside the reduction)
@@ -1024,7 +839,6 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
     const int row = (warp & 3) * 32 + static_cast<int>(lane);
     cluster_arrive();
     cluster_wait();
-    if (threadIdx.x == 0) DMARK(34);
     if (scale && rank > 0) {
       const uint32_t dst = mapa_shared(w0 + ((rank - 1) * NT * 128 + row) * 4, 0);
 #pragma unroll
@@ -1032,7 +846,6 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
     }
     cluster_arrive();
     cluster_wait();
-    if (threadIdx.x == 0) DMARK(35);
     if (scale && rank == 0) {
       const float* red = reinterpret_cast<const float*>(w_ptr0);
       for (int q = 1; q < CS; ++q) {
@@ -1048,15 +861,6 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
         if (m < mcount) dec_store<BF16, OUT>(args.out, args.N, mb + m, n, acc_keep[m]);
     }
   }
-#if TM_PROFILE
-  // CTA end (slot 6): after the teardown and the cluster reduction, once every warp is done
-  __syncthreads();
-  if (args.trace && threadIdx.x == 0) {
-    uint64_t gt;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    args.trace[blockIdx.x * 160 + 6] = static_cast<uint32_t>(gt);
-  }
-#endif
 }
 
 #undef DEC_FOR_SEGMENTS
