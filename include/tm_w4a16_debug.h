@@ -35,6 +35,11 @@ tm_status tm_query_gemm_kind(int M, int N, int K, int* kind);
  * chunks), split < 0 its stream-K mode with -split CTAs, 0 = automatic.                     */
 tm_status tm_set_decode_path(int path, int split);
 
+/* Prefill (M >= 1024, bf16/fp16 output): on != 0 runs the persistent kernel (gemm_pk.cuh: one
+ * CTA per SM over 128 x 192 tiles, double-buffered TMEM accumulator, kind 4) instead of the
+ * tiled kernel (kind 0, the default: measured faster on every CFG#2 shape).                  */
+tm_status tm_set_prefill_persistent(int on);
+
 /* Decode cluster mode: 0 automatic (default), 1 never (always stream-K), 2..8 force that many
  * CTAs per tile (capped by shared memory and K), -1 one CTA per tile without a split.        */
 tm_status tm_set_decode_cluster(int cs);

@@ -71,6 +71,7 @@ _SIGS = {
     "tm_query_gemm_kind": (_I, [_I, _I, _I, ctypes.POINTER(_I)]),
     "tm_set_decode_cluster": (_I, [_I]),
     "tm_set_decode_path": (_I, [_I, _I]),
+    "tm_set_prefill_persistent": (_I, [_I]),
     "tm_set_trace": (_I, [_P, ctypes.c_int64]),
     "tm_status_string": (ctypes.c_char_p, [_I]),
     "tm_version": (ctypes.c_char_p, []),
@@ -384,6 +385,11 @@ def set_decode_path(path=0, split=0):
     decode kernel, 2 register-fed; split in 1..8 forces the register-fed kernel's cluster split,
     split < 0 its stream-K CTA count."""
     _check(lib().tm_set_decode_path(path, split))
+
+
+def set_prefill_persistent(on=True):
+    """Tests/benchmarks: run the persistent prefill kernel (kind 4) for M >= 1024."""
+    _check(lib().tm_set_prefill_persistent(1 if on else 0))
 
 
 def set_trace(buf=None):

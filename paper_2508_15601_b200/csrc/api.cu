@@ -17,6 +17,7 @@
 #include "gemm_w4a16.cuh"
 #include "gemm_dec.cuh"
 #include "gemm_rf.cuh"
+#include "gemm_pk.cuh"
 #include "attn_dec.cuh"
 #include "tp_reduce.cuh"
 
@@ -348,7 +349,8 @@ tm_status get_workspace(cudaStream_t stream, void* user, int64_t user_bytes, int
 
 // ---------------------------------------------------------------- launch configuration
 struct Config {
-  int kind;  // 0 = classic tiles (+ cluster split-K), 1 = persistent stream-K, 3 = register-fed
+  int kind;  // 0 = classic tiles (+ cluster split-K), 1 = persistent stream-K, 4 = persistent
+             // prefill (gemm_pk.cuh), 3 = register-fed
              // decode kernel (split = CTAs per tile), 2 = decode kernel
              // with CS CTAs per tile reduced over a thread-block cluster (split = CS)
   int NT;
@@ -557,8 +559,35 @@ Config rf_config(int M, int N, int K) {
 // slower on gate_up/down and at M = 16, so automatic dispatch keeps the TMEM kernel.
 bool use_rf(int M) { return M <= 16 && g_dec_path.load() == 2; }
 
+// Persistent prefill kernel (gemm_pk.cuh, kind 4): 128 x 192 tiles, one CTA per SM walking the
+// tiles, double-buffered TMEM accumulator, for M >= kPkMinM (bf16/fp16 outputs; fp32 partials keep
+// the tiled kernel).  Opt-in (tm_set_prefill_persistent): measured 7-30 % slower than the tiled
+// kernel on every CFG#2 shape -- the stage loads, not the per-tile overheads, bound it.
+constexpr int kPkNT = 192;
+constexpr int kPkMinM = 1024;
+std::atomic<int> g_pk{0};
+bool use_pk(int M) {
+  return g_pk.load() != 0 && M >= kPkMinM && g_override_tile.load() == 0 && g_override_split.load() == 0;
+}
+Config pk_config(int M, int N) {
+  Config c{};
+  c.kind = 4;
+  c.NT = kPkNT;
+  c.split = 1;
+  const long long tiles = static_cast<long long>(N / 128) * ((M + kPkNT - 1) / kPkNT);
+  c.grid_x = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
+  c.grid_y = 1;
+  return c;
+}
+
+Config choose_config_tiled(int M, int N, int K);
 Config choose_config(int M, int N, int K) {
   if (use_rf(M)) return rf_config(M, N, K);
+  if (use_pk(M)) return pk_config(M, N);
+  return choose_config_tiled(M, N, K);
+}
+
+Config choose_config_tiled(int M, int N, int K) {
   Config c{};
   int nt = 16;
   const int ot = g_override_tile.load();
@@ -804,6 +833,41 @@ tm_status launch_gemm(const CUtensorMap& map, const GemmArgs& args, const Config
   }
 }
 
+template <bool BF16>
+tm_status launch_pk(const void* A, const GemmArgs& args, const Config& c, cudaStream_t stream) {
+  constexpr int NT = kPkNT;
+  using Cfg = PkCfg<NT, BF16>;
+  auto kern = w4a16_gemm_pk_kernel<NT, BF16>;
+  static std::atomic<int> configured[kMaxDevices] = {};
+  tm_status st = ensure_smem(kern, Cfg::SMEM, configured);
+  if (st != TM_OK) return st;
+  CUtensorMap amap, cmap, smap, zmap;
+  st = act_tensor_map(A, args.M, args.a_ks * 64, NT, BF16, &amap);
+  if (st != TM_OK) return st;
+  st = out_tensor_map(args.out, args.M, args.N, NT, 2, BF16, &cmap);
+  if (st != TM_OK) return st;
+  st = sz_tensor_map(args.scales, args.K / args.group, args.N, &smap);
+  if (st != TM_OK) return st;
+  st = sz_tensor_map(args.zeros, args.K / args.group, args.N, &zmap);
+  if (st != TM_OK) return st;
+  const int n_tiles = args.N / 128, m_tiles = (args.M + NT - 1) / NT;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(c.grid_x, 1, 1);
+  cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, amap, cmap, smap, zmap, args, n_tiles, m_tiles) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return TM_ERR_CUDA;
+  }
+  return TM_OK;
+}
+
 template <int NT, int GROUP, bool BF16, int OUT>
 tm_status launch_rf_t(const void* A, const GemmArgs& g, const Config& c, cudaStream_t stream, UserWs ws) {
   using Cfg = RfCfg<NT, GROUP>;
@@ -890,7 +954,8 @@ tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* sca
   if (!A || !C) return TM_ERR_INVALID_ARG;
   if (!aligned16(A) || !aligned16(packed->data) || !aligned16(scales) || !aligned16(zeros) || !aligned16(C))
     return TM_ERR_MISALIGNED;
-  const Config c = choose_config(M, N, K);
+  Config c = choose_config(M, N, K);
+  if (c.kind == 4 && out_kind == OUT_F32) c = choose_config_tiled(M, N, K);  // fp32 partials: tiled kernel
   GemmArgs args;
   args.packed = static_cast<const uint8_t*>(packed->data);
   args.scales = static_cast<const uint16_t*>(scales);
@@ -916,6 +981,7 @@ tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* sca
   }
   args.trace = g_trace;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c.kind == 4) return bf16 ? launch_pk<true>(A, args, c, s) : launch_pk<false>(A, args, c, s);
   if (c.kind == 3) {
     if (out_kind == OUT_F32) return launch_rf<true, OUT_F32>(A, args, c, s, ws);
     return bf16 ? launch_rf<true, OUT_ACT>(A, args, c, s, ws) : launch_rf<false, OUT_ACT>(A, args, c, s, ws);
@@ -1350,6 +1416,11 @@ tm_status tm_query_gemm_config(int M, int N, int K, int* tile_m, int* split_k, i
 tm_status tm_query_gemm_kind(int M, int N, int K, int* kind) {
   if (M <= 0 || N <= 0 || K <= 0 || N % 128 || K % 64 || !kind) return TM_ERR_INVALID_ARG;
   *kind = choose_config(M, N, K).kind;
+  return TM_OK;
+}
+
+tm_status tm_set_prefill_persistent(int on) {
+  g_pk.store(on ? 1 : 0);
   return TM_OK;
 }
 
