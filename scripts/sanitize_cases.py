@@ -85,4 +85,36 @@ if only is None or only == "extra":
     refa = decode_attention_f64(pr["Q"], pr["kq"], pr["ks"], pr["kz"], pr["vq"], pr["vs"], pr["vz"], pr["seq_lens"])
     ok &= compare.relfro(O.float().cpu().numpy(), refa) < 5e-3
     print("attention", ok, flush=True)
+if only is None or only == "extra" or only == "r2":
+    # round-2 opt-in kernels: register-fed decode (cluster split and stream-K), persistent prefill,
+    # fused TP all-reduce + finalize (one rank, pre-signalled peers)
+    for split in (3, -5):
+        api.set_decode_path(2, split)
+        d = synth.awq_like(9, 384, 1280, group=128, seed=70 + split)
+        A = torch.from_numpy(d["A"]).to(torch.bfloat16).cuda()
+        q, s_, z = (torch.from_numpy(d[k]).cuda() for k in ("q", "s", "z"))
+        C = api.gemm_w4a16(A, api.pack_w4(q, s_, z, 128), s_, z)
+        torch.cuda.synchronize()
+        ok &= compare.relfro(C.float().cpu().numpy(), gemm_f64(d["A"], d["q"], d["s"], d["z"], 128)) < 5e-3
+        print("rf", split, ok, flush=True)
+    api.set_decode_path(0, 0)
+    api.set_prefill_persistent(True)
+    d = synth.awq_like(1100, 256, 512, group=64, seed=71)
+    A = torch.from_numpy(d["A"]).to(torch.bfloat16).cuda()
+    q, s_, z = (torch.from_numpy(d[k]).cuda() for k in ("q", "s", "z"))
+    C = api.gemm_w4a16(A, api.pack_w4(q, s_, z, 64), s_, z)
+    torch.cuda.synchronize()
+    ok &= compare.relfro(C.float().cpu().numpy(), gemm_f64(d["A"], d["q"], d["s"], d["z"], 64)) < 5e-3
+    api.set_prefill_persistent(False)
+    print("pk", ok, flush=True)
+    P_, rank = 2, 1
+    parts = [torch.randn(1027, device="cuda") for _ in range(P_)]
+    pads = [torch.zeros(64 * P_, dtype=torch.int32, device="cuda") for _ in range(P_)]
+    for ch in range(64):
+        pads[rank][ch * P_ + 0] = 1
+    out = torch.empty(1027, dtype=torch.bfloat16, device="cuda")
+    api.tp_allreduce_finalize([t.data_ptr() for t in parts], [t.data_ptr() for t in pads], 0, rank, P_, 1027, out)
+    torch.cuda.synchronize()
+    ok &= bool(torch.equal(out, (parts[0] + parts[1]).to(torch.bfloat16)))
+    print("tp_reduce", ok, flush=True)
 print("all ok" if ok else "FAILURES")
