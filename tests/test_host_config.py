@@ -57,3 +57,52 @@ def test_prefill_full_tiles(M, N, K):
     tiles = (N // 128) * ((M + 255) // 256)
     assert c["split_k"] == (1 if tiles > 64 else c["split_k"])
     assert c["grid_ctas"] == tiles * c["split_k"]
+
+
+@pytest.mark.parametrize("M", [1, 8, 9, 16])
+@pytest.mark.parametrize("N,K", SHAPES_8B + SHAPES_70B + MIXTRAL + [(8192, 29568)])
+def test_register_fed_configs(M, N, K):
+    """Opt-in register-fed decode kernel (kind 3): cluster split for few tiles (S <= 8 CTAs per
+    tile, >= 2 chunks each, one wave at two CTAs per SM), stream-K over 2 x SMs CTAs otherwise;
+    32-bit range math (tiles x chunks x CTAs < 2^32)."""
+    api.set_decode_path(2, 0)
+    try:
+        c = api.query_gemm_config(M, N, K)
+    finally:
+        api.set_decode_path(0, 0)
+    tiles, kc = N // 128, (K + 255) // 256
+    assert c["kind"] == 3 and c["tile_m"] == (8 if M <= 8 else 16)
+    if c["split_k"] > 0:
+        S = c["split_k"]
+        assert tiles <= SMS and 1 <= S <= 8 and c["grid_ctas"] == tiles * S <= 2 * SMS
+        assert S == 1 or kc >= 2 * S
+    else:
+        P = -c["split_k"]
+        assert tiles > SMS and P == c["grid_ctas"] == min(2 * SMS, tiles * kc)
+        assert tiles * kc * P < 2 ** 32
+    assert api.query_gemm_config(M, N, K)["kind"] in (1, 2)  # the default path is the TMEM kernel
+
+
+@pytest.mark.parametrize("M", [1024, 2048, 8192])
+@pytest.mark.parametrize("N,K", SHAPES_8B)
+def test_persistent_prefill_opt_in(M, N, K):
+    assert api.query_gemm_config(M, N, K)["kind"] == 0  # default: the tiled kernel
+    api.set_prefill_persistent(True)
+    try:
+        c = api.query_gemm_config(M, N, K)
+    finally:
+        api.set_prefill_persistent(False)
+    tiles = (N // 128) * ((M + 191) // 192)
+    assert c["kind"] == 4 and c["tile_m"] == 192 and c["grid_ctas"] == min(SMS, tiles)
+
+
+def test_tp_allreduce_finalize_rejects_bad_arguments_without_a_device():
+    """Argument validation happens before any CUDA call (runs on the CPU box)."""
+    import ctypes
+    lib = api.lib()
+    P = (ctypes.c_void_p * 2)(16, 32)
+    S = (ctypes.c_void_p * 2)(64, 128)
+    for rank, world in ((0, 0), (2, 2), (0, 9), (-1, 2)):
+        assert lib.tm_tp_allreduce_finalize(P, S, None, rank, world, 8, ctypes.c_void_p(256), None) != 0
+    P1 = (ctypes.c_void_p * 1)(20)  # misaligned partial
+    assert lib.tm_tp_allreduce_finalize(P1, S, None, 0, 1, 8, ctypes.c_void_p(256), None) != 0
