@@ -559,6 +559,8 @@ Config rf_config(int M, int N, int K) {
 // slower on gate_up/down and at M = 16, so automatic dispatch keeps the TMEM kernel.
 bool use_rf(int M) { return M <= 16 && g_dec_path.load() == 2; }
 
+
+
 // Persistent prefill kernel (gemm_pk.cuh, kind 4): 128 x 192 tiles, one CTA per SM walking the
 // tiles, double-buffered TMEM accumulator, for M >= kPkMinM (bf16/fp16 outputs; fp32 partials keep
 // the tiled kernel).  Opt-in (tm_set_prefill_persistent): measured 7-30 % slower than the tiled

@@ -191,6 +191,97 @@ __device__ __forceinline__ void rf_store(void* out, size_t idx, float v) {
     reinterpret_cast<__half*>(out)[idx] = __float2half_rn(v);
 }
 
+// One 256-k chunk for consumer warp cw (columns 32 cw .. 32 cw + 31 of the tile): B fragments
+// from the activation stage, weight fragments by ldmatrix from the weight stage, I2F magic,
+// mma.sync per group, then acc += s D' - s (V + z) R in fp32 (reading R6c).  nbv = valid blobs.
+template <int NT, int GROUP, bool BF16>
+__device__ __forceinline__ void rf_chunk(float (&acc)[2][NT / 8][4], uint32_t ast, uint32_t wst, const float* R,
+                                         int nbv, int cw, int lane) {
+  using Cfg = RfCfg<NT, GROUP>;
+  constexpr int NOCT = Cfg::NOCT, U = Cfg::U, BPG = Cfg::BPG;
+  constexpr float V = BF16 ? 128.0f : 1024.0f;
+  const int g = lane >> 2, c = lane & 3;
+  const int sig = (g >> 1) | ((g & 1) << 2);
+  const uint32_t lm_off =
+      static_cast<uint32_t>((lane >> 4) * 2048 + (((lane >> 3) & 1) * 8 + (lane & 7)) * 16 + cw * 2 * 256);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (u * BPG < nbv) {
+        constexpr int NCH = TM_RF_CHAIN ? 2 : 1;  // accumulator chains per row group
+        float dd[NCH][2][NOCT][4];
+#pragma unroll
+        for (int q = 0; q < NCH; ++q)
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int o = 0; o < NOCT; ++o)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) dd[q][r][o][e] = 0.f;
+#pragma unroll
+        for (int bb = 0; bb < BPG; ++bb) {
+          const int blob = u * BPG + bb;
+          uint4 bfr[2][NOCT];
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int o = 0; o < NOCT; ++o) {
+              const int row = sig + 8 * o;
+              bfr[j][o] = rf_lds128(ast + blob * (NT * 128) + row * 128 + (((4 * j + c) ^ (row & 7)) << 4));
+            }
+          uint32_t wv[2][4];
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+            rf_ldmatrix_x4(wst + blob * 4096 + lm_off + r * 256, wv[r]);
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+              uint32_t p0[4], p1[4];
+              rf_magic<BF16>(wv[r][2 * j], p0);      // column 16 rg + g
+              rf_magic<BF16>(wv[r][2 * j + 1], p1);  // column 16 rg + g + 8
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const uint32_t a[4] = {p0[2 * h], p1[2 * h], p0[2 * h + 1], p1[2 * h + 1]};
+#pragma unroll
+                for (int o = 0; o < NOCT; ++o)
+                  rf_hmma<BF16>(dd[j % NCH][r][o], a, h ? bfr[j][o].z : bfr[j][o].x, h ? bfr[j][o].w : bfr[j][o].y);
+              }
+            }
+        }
+        float d[2][NOCT][4];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int o = 0; o < NOCT; ++o)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) d[r][o][e] = NCH == 2 ? dd[0][r][o][e] + dd[NCH - 1][r][o][e] : dd[0][r][o][e];
+        // group end: C += s D' - s (V + z) R  (fp32)
+        float rr[NOCT][2];
+#pragma unroll
+        for (int o = 0; o < NOCT; ++o) {
+          const float2 tv = *reinterpret_cast<const float2*>(R + ((u * 4 + c) * NOCT + o) * 2);
+          rr[o][0] = tv.x;  // token c + 8 o
+          rr[o][1] = tv.y;  // token c + 4 + 8 o
+        }
+        const uint32_t ssm = ast + Cfg::A_BYTES + u * 256;  // fp16 s[col] of group u
+        const uint32_t zsm = ssm + Cfg::SZ_BYTES;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const uint32_t col0 = static_cast<uint32_t>(16 * (2 * cw + r) + g) * 2;
+          const float s0 = rf_lds_h2f(ssm + col0), s1 = rf_lds_h2f(ssm + col0 + 16);
+          const float sv0 = -s0 * (V + rf_lds_h2f(zsm + col0)), sv1 = -s1 * (V + rf_lds_h2f(zsm + col0 + 16));
+#pragma unroll
+          for (int o = 0; o < NOCT; ++o) {
+            acc[r][o][0] = fmaf(s0, d[r][o][0], fmaf(sv0, rr[o][0], acc[r][o][0]));
+            acc[r][o][1] = fmaf(s0, d[r][o][1], fmaf(sv0, rr[o][1], acc[r][o][1]));
+            acc[r][o][2] = fmaf(s1, d[r][o][2], fmaf(sv1, rr[o][0], acc[r][o][2]));
+            acc[r][o][3] = fmaf(s1, d[r][o][3], fmaf(sv1, rr[o][1], acc[r][o][3]));
+          }
+        }
+      }
+    }
+}
+
 // ring position of the i-th chunk of a CTA in an N-slot ring
 template <int N>
 struct RfSlot {
@@ -384,83 +475,7 @@ __global__ void __launch_bounds__(RfCfg<NT, GROUP>::THREADS, RfCfg<NT, GROUP>::M
       const uint32_t ast = aring + sa.slot * Cfg::AS_BYTES;
       const float* const R = reinterpret_cast<const float*>(base_ptr + Cfg::OFF_A + sa.slot * Cfg::AS_BYTES +
                                                             Cfg::A_BYTES + 2 * Cfg::SZ_BYTES);
-      const int nbv = KS - static_cast<int>(cc) * 4;  // valid blobs of the chunk (>= 4: full)
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (u * BPG < nbv) {
-          constexpr int NCH = TM_RF_CHAIN ? 2 : 1;  // accumulator chains per row group
-          float dd[NCH][2][NOCT][4];
-#pragma unroll
-          for (int q = 0; q < NCH; ++q)
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-              for (int o = 0; o < NOCT; ++o)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) dd[q][r][o][e] = 0.f;
-#pragma unroll
-          for (int bb = 0; bb < BPG; ++bb) {
-            const int blob = u * BPG + bb;
-            uint4 bfr[2][NOCT];
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-              for (int o = 0; o < NOCT; ++o) {
-                const int row = sig + 8 * o;
-                bfr[j][o] = rf_lds128(ast + blob * (NT * 128) + row * 128 + (((4 * j + c) ^ (row & 7)) << 4));
-              }
-            uint32_t wv[2][4];
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-              rf_ldmatrix_x4(wring + sw.slot * Cfg::W_BYTES + blob * 4096 + lm_off + r * 256, wv[r]);
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-              for (int r = 0; r < 2; ++r) {
-                uint32_t p0[4], p1[4];
-                rf_magic<BF16>(wv[r][2 * j], p0);      // column 16 rg + g
-                rf_magic<BF16>(wv[r][2 * j + 1], p1);  // column 16 rg + g + 8
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  const uint32_t a[4] = {p0[2 * h], p1[2 * h], p0[2 * h + 1], p1[2 * h + 1]};
-#pragma unroll
-                  for (int o = 0; o < NOCT; ++o)
-                    rf_hmma<BF16>(dd[j % NCH][r][o], a, h ? bfr[j][o].z : bfr[j][o].x, h ? bfr[j][o].w : bfr[j][o].y);
-                }
-              }
-          }
-          float d[2][NOCT][4];
-#pragma unroll
-          for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int o = 0; o < NOCT; ++o)
-#pragma unroll
-              for (int e = 0; e < 4; ++e) d[r][o][e] = NCH == 2 ? dd[0][r][o][e] + dd[NCH - 1][r][o][e] : dd[0][r][o][e];
-          // group end: C += s D' - s (V + z) R  (fp32)
-          float rr[NOCT][2];
-#pragma unroll
-          for (int o = 0; o < NOCT; ++o) {
-            const float2 tv = *reinterpret_cast<const float2*>(R + ((u * 4 + c) * NOCT + o) * 2);
-            rr[o][0] = tv.x;  // token c + 8 o
-            rr[o][1] = tv.y;  // token c + 4 + 8 o
-          }
-          const uint32_t ssm = ast + Cfg::A_BYTES + u * 256;  // fp16 s[col] of group u
-          const uint32_t zsm = ssm + Cfg::SZ_BYTES;
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const uint32_t col0 = static_cast<uint32_t>(16 * (2 * cw + r) + g) * 2;
-            const float s0 = rf_lds_h2f(ssm + col0), s1 = rf_lds_h2f(ssm + col0 + 16);
-            const float sv0 = -s0 * (V + rf_lds_h2f(zsm + col0)), sv1 = -s1 * (V + rf_lds_h2f(zsm + col0 + 16));
-#pragma unroll
-            for (int o = 0; o < NOCT; ++o) {
-              acc[r][o][0] = fmaf(s0, d[r][o][0], fmaf(sv0, rr[o][0], acc[r][o][0]));
-              acc[r][o][1] = fmaf(s0, d[r][o][1], fmaf(sv0, rr[o][1], acc[r][o][1]));
-              acc[r][o][2] = fmaf(s1, d[r][o][2], fmaf(sv1, rr[o][0], acc[r][o][2]));
-              acc[r][o][3] = fmaf(s1, d[r][o][3], fmaf(sv1, rr[o][1], acc[r][o][3]));
-            }
-          }
-        }
-      }
+      rf_chunk<NT, GROUP, BF16>(acc, ast, wring + sw.slot * Cfg::W_BYTES, R, KS - static_cast<int>(cc) * 4, cw, lane);
     }
     __syncwarp();
     if (lane == 0) {
@@ -609,5 +624,7 @@ __global__ void __launch_bounds__(RfCfg<NT, GROUP>::THREADS, RfCfg<NT, GROUP>::M
   }
   if (threadIdx.x == 96) rf_mark(args.trace, 4);
 }
+
+
 
 }  // namespace w4k

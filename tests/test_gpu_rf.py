@@ -170,3 +170,4 @@ def test_w8a16_bit_planes():
     W = (q8.astype(np.float64) - np.repeat(z8.astype(np.float64), g, axis=0)) * np.repeat(s.astype(np.float64), g, axis=0)
     ref = A.astype(np.float64) @ W
     assert compare.relfro(to_np64(C), ref) <= compare.RELFRO_TOL
+
