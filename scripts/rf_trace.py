@@ -50,3 +50,13 @@ for cta in [0, 1, G // 3, G // 2, G - 1]:
     ch = [rel(x) for x in t[cta, 8:56] if x != 0]
     print(f"cta {cta:4d}: start {rel(t[cta,0]):6.2f} setup {rel(t[cta,1]):6.2f} gdw {rel(t[cta,2]):6.2f} chunks " +
           " ".join(f"{x:.2f}" for x in ch[:30]) + f" | loopend {rel(t[cta,3]):.2f} t5 {rel(t[cta,5]):.2f} t6 {rel(t[cta,6]):.2f} t7 {rel(t[cta,7]):.2f} end {rel(t[cta,4]):.2f}")
+ends = rel(t[:, 3])
+h = G // 2
+if G > 148:
+    print("loop end by placement: first %d CTAs med %.2f p90 %.2f max %.2f | rest med %.2f p90 %.2f max %.2f" % (
+        min(148, G), np.median(ends[:148]), np.percentile(ends[:148], 90), ends[:148].max(),
+        np.median(ends[148:]), np.percentile(ends[148:], 90), ends[148:].max()))
+first = rel(t[:, 8])
+print("first chunk done: med %.2f p90 %.2f max %.2f" % (np.median(first), np.percentile(first, 90), first.max()))
+slow = np.argsort(-ends)[:12]
+print("slowest CTAs:", " ".join(f"{i}:{ends[i]:.1f}" for i in slow))
