@@ -26,7 +26,9 @@ tm_status tm_query_gemm_config(int M, int N, int K, int* tile_m, int* split_k, i
  * K in one cluster, chosen for 65 <= M <= 512 while tiles * split_k <= 128), 1 = persistent
  * stream-K decode, 2 = decode with split_k CTAs per tile reduced in distributed shared memory
  * over a thread-block cluster (split_k = 1: one CTA per tile), 3 = register-fed decode
- * (M <= 16; split_k CTAs per tile reduced through the workspace in CTA order).              */
+ * (M <= 16; split_k CTAs per tile reduced through the workspace in CTA order), 4 = persistent
+ * prefill (opt-in), 5 = prefill on CTA pairs (cta_group::2; grid_ctas CTAs = grid_ctas / 2
+ * pairs of 256 weight columns x 256 tokens).                                                 */
 tm_status tm_query_gemm_kind(int M, int N, int K, int* kind);
 
 /* Decode kernel for M <= 16: path 0 = automatic (the TMEM decode kernel, kinds 1/2), 1 = the
@@ -37,8 +39,15 @@ tm_status tm_set_decode_path(int path, int split);
 
 /* Prefill (M >= 1024, bf16/fp16 output): on != 0 runs the persistent kernel (gemm_pk.cuh: one
  * CTA per SM over 128 x 192 tiles, double-buffered TMEM accumulator, kind 4) instead of the
- * tiled kernel (kind 0, the default: measured faster on every CFG#2 shape).                  */
+ * tiled kernel (kind 0) or the pair kernel (kind 5) -- both measured faster on every CFG#2
+ * shape.                                                                                     */
 tm_status tm_set_prefill_persistent(int on);
+
+/* Prefill on CTA pairs (gemm_2sm.cuh, kind 5, tcgen05 cta_group::2): chosen by default where
+ * the tiled kernel would run 256-token tiles without split-K and N % 256 == 0, for bf16/fp16
+ * outputs (fp32 partials keep the tiled kernel).  on = 0 restores the tiled kernel (kind 0)
+ * there -- A/B measurements and tests.  Default 1.                                           */
+tm_status tm_set_prefill_pair(int on);
 
 /* Decode cluster mode: 0 automatic (default), 1 never (always stream-K), 2..8 force that many
  * CTAs per tile (capped by shared memory and K), -1 one CTA per tile without a split.        */

@@ -72,6 +72,7 @@ _SIGS = {
     "tm_set_decode_cluster": (_I, [_I]),
     "tm_set_decode_path": (_I, [_I, _I]),
     "tm_set_prefill_persistent": (_I, [_I]),
+    "tm_set_prefill_pair": (_I, [_I]),
     "tm_set_trace": (_I, [_P, ctypes.c_int64]),
     "tm_status_string": (ctypes.c_char_p, [_I]),
     "tm_version": (ctypes.c_char_p, []),
@@ -390,6 +391,11 @@ def set_decode_path(path=0, split=0):
 def set_prefill_persistent(on=True):
     """Tests/benchmarks: run the persistent prefill kernel (kind 4) for M >= 1024."""
     _check(lib().tm_set_prefill_persistent(1 if on else 0))
+
+
+def set_prefill_pair(on=True):
+    """Tests/benchmarks: CTA-pair prefill kernel (kind 5, the default where it applies) on/off."""
+    _check(lib().tm_set_prefill_pair(1 if on else 0))
 
 
 def set_trace(buf=None):

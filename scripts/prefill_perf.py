@@ -1,5 +1,6 @@
-"""Prefill (tiled kernel) timing per shape, CUDA-graph replay, with torch.matmul bf16 beside it.
-python scripts/prefill_perf.py [--ms 2048,4096,8192]"""
+"""Prefill timing per shape (the default dispatch: CTA-pair kernel where it applies), CUDA-graph
+replay, with torch.matmul bf16 beside it; --ab also times the tiled kernel (tm_set_prefill_pair(0))
+in the same process, interleaved.   python scripts/prefill_perf.py [--ms 2048,4096,8192] [--ab]"""
 import argparse
 import os
 import sys
@@ -35,6 +36,7 @@ def gtime(fn, reps=5):
 ap = argparse.ArgumentParser()
 ap.add_argument("--ms", default="2048,4096,8192")
 ap.add_argument("--shapes", default="qkv,o,gate_up,down")
+ap.add_argument("--ab", action="store_true")
 a = ap.parse_args()
 for name in a.shapes.split(","):
     N, K = SHAPES[name]
@@ -44,8 +46,15 @@ for name in a.shapes.split(","):
     for M in [int(x) for x in a.ms.split(",")]:
         A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
         C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        kind = api.query_gemm_config(M, N, K)["kind"]
         t = gtime(lambda: api.gemm_w4a16(A, p, d["s"], d["z"], out=C))
         td = gtime(lambda: torch.matmul(A, W, out=C))
         fl = 2 * M * N * K
-        print(f"  {name:8s} M={M:5d}  w4a16 {t:8.1f} us {fl / t / 1e6:7.1f} TF/s   torch bf16 {td:8.1f} us "
-              f"{fl / td / 1e6:7.1f} TF/s   ratio {td / t:5.2f}", flush=True)
+        extra = ""
+        if a.ab:
+            api.set_prefill_pair(False)
+            tt = gtime(lambda: api.gemm_w4a16(A, p, d["s"], d["z"], out=C))
+            api.set_prefill_pair(True)
+            extra = f"   tiled {tt:8.1f} us ratio {td / tt:5.2f}"
+        print(f"  {name:8s} M={M:5d}  w4a16(kind {kind}) {t:8.1f} us {fl / t / 1e6:7.1f} TF/s   torch bf16 {td:8.1f} us "
+              f"{fl / td / 1e6:7.1f} TF/s   ratio {td / t:5.2f}{extra}", flush=True)

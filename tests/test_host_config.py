@@ -34,8 +34,9 @@ def test_decode_configs_fit_one_wave(M, N, K):
 @pytest.mark.parametrize("N,K", SHAPES_8B + SHAPES_70B)
 def test_mid_m_cluster_split(M, N, K):
     c = api.query_gemm_config(M, N, K)
-    assert c["kind"] == 0
     nt = c["tile_m"]
+    # 256-token tiles without a split run on CTA pairs (kind 5) when N % 256 == 0
+    assert c["kind"] == (5 if nt == 256 and c["split_k"] == 1 and N % 256 == 0 else 0)
     if M <= 128:
         assert nt == 128
     elif M <= 256:
@@ -53,7 +54,8 @@ def test_mid_m_cluster_split(M, N, K):
 @pytest.mark.parametrize("N,K", SHAPES_8B + SHAPES_70B)
 def test_prefill_full_tiles(M, N, K):
     c = api.query_gemm_config(M, N, K)
-    assert (c["kind"], c["tile_m"]) == (0, 256)
+    assert c["tile_m"] == 256
+    assert c["kind"] == (5 if c["split_k"] == 1 and N % 256 == 0 else 0)
     tiles = (N // 128) * ((M + 255) // 256)
     assert c["split_k"] == (1 if tiles > 64 else c["split_k"])
     assert c["grid_ctas"] == tiles * c["split_k"]
@@ -86,7 +88,7 @@ def test_register_fed_configs(M, N, K):
 @pytest.mark.parametrize("M", [1024, 2048, 8192])
 @pytest.mark.parametrize("N,K", SHAPES_8B)
 def test_persistent_prefill_opt_in(M, N, K):
-    assert api.query_gemm_config(M, N, K)["kind"] == 0  # default: the tiled kernel
+    assert api.query_gemm_config(M, N, K)["kind"] == 5  # default: the CTA-pair kernel
     api.set_prefill_persistent(True)
     try:
         c = api.query_gemm_config(M, N, K)
@@ -94,6 +96,21 @@ def test_persistent_prefill_opt_in(M, N, K):
         api.set_prefill_persistent(False)
     tiles = (N // 128) * ((M + 191) // 192)
     assert c["kind"] == 4 and c["tile_m"] == 192 and c["grid_ctas"] == min(SMS, tiles)
+
+
+@pytest.mark.parametrize("M", [1024, 4096])
+@pytest.mark.parametrize("N,K", SHAPES_8B + SHAPES_70B + [(384, 4096), (640, 2048)])
+def test_pair_prefill_dispatch(M, N, K):
+    """Kind 5 (CTA pairs) exactly where the tiled chooser picks unsplit 256-token tiles and
+    N % 256 == 0; tm_set_prefill_pair(0) restores the tiled kernel with the same grid."""
+    c = api.query_gemm_config(M, N, K)
+    assert c["kind"] == (5 if N % 256 == 0 and c["split_k"] == 1 else 0)
+    api.set_prefill_pair(False)
+    try:
+        t = api.query_gemm_config(M, N, K)
+    finally:
+        api.set_prefill_pair(True)
+    assert t["kind"] == 0 and (t["tile_m"], t["split_k"], t["grid_ctas"]) == (c["tile_m"], c["split_k"], c["grid_ctas"])
 
 
 def test_tp_allreduce_finalize_rejects_bad_arguments_without_a_device():
