@@ -44,8 +44,8 @@ tm_status tm_set_decode_path(int path, int split);
 tm_status tm_set_prefill_persistent(int on);
 
 /* Prefill on CTA pairs (gemm_2sm.cuh, kind 5, tcgen05 cta_group::2): chosen by default where
- * the tiled kernel would run 256-token tiles without split-K and N % 256 == 0, for bf16/fp16
- * outputs (fp32 partials keep the tiled kernel).  on = 0 restores the tiled kernel (kind 0)
+ * the tiled kernel would run 256-token tiles without split-K and N % 256 == 0 (bf16/fp16
+ * outputs and fp32 partials).  on = 0 restores the tiled kernel (kind 0)
  * there -- A/B measurements and tests.  Default 1.                                           */
 tm_status tm_set_prefill_pair(int on);
 

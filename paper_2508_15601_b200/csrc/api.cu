@@ -584,7 +584,7 @@ Config pk_config(int M, int N) {
 }
 
 // CTA-pair prefill kernel (gemm_2sm.cuh, kind 5): where the tiled chooser picks 256-token tiles
-// without split-K and N % 256 == 0 (bf16/fp16 outputs; fp32 partials keep the tiled kernel).
+// without split-K and N % 256 == 0 (bf16/fp16 outputs and fp32 partials).
 // Measured 4-9 % faster than the tiled kernel on every CFG#2 shape; on by
 // default, tm_set_prefill_pair(0) restores the tiled kernel (A/B, tests).
 std::atomic<int> g_pair{1};
@@ -849,16 +849,16 @@ tm_status launch_gemm(const CUtensorMap& map, const GemmArgs& args, const Config
 
 // CTA-pair prefill (gemm_2sm.cuh): where the tiled kernel would run 128 x 256 tiles without
 // split-K, N % 256 == 0, bf16/fp16 output.
-template <bool BF16>
+template <bool BF16, int OUT>
 tm_status launch_2sm(const void* A, const GemmArgs& args, cudaStream_t stream) {
-  auto kern = w4a16_gemm_2sm_kernel<BF16>;
+  auto kern = w4a16_gemm_2sm_kernel<BF16, OUT>;
   static std::atomic<int> configured[kMaxDevices] = {};
   tm_status st = ensure_smem(kern, Pair2Cfg::SMEM, configured);
   if (st != TM_OK) return st;
   CUtensorMap amap, cmap, smap, zmap;
   st = act_tensor_map(A, args.M, args.a_ks * 64, Pair2Cfg::HALF, BF16, &amap);
   if (st != TM_OK) return st;
-  st = out_tensor_map(args.out, args.M, args.N, Pair2Cfg::NT, 2, BF16, &cmap);
+  st = out_tensor_map(args.out, args.M, args.N, Pair2Cfg::NT, OUT == OUT_F32 ? 4 : 2, BF16, &cmap);
   if (st != TM_OK) return st;
   st = sz_tensor_map(args.scales, args.K / args.group, args.N, &smap);
   if (st != TM_OK) return st;
@@ -1007,7 +1007,7 @@ tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* sca
   if (!aligned16(A) || !aligned16(packed->data) || !aligned16(scales) || !aligned16(zeros) || !aligned16(C))
     return TM_ERR_MISALIGNED;
   Config c = choose_config(M, N, K);
-  if ((c.kind == 4 || c.kind == 5) && out_kind == OUT_F32) c = choose_config_tiled(M, N, K);  // fp32: tiled
+  if (c.kind == 4 && out_kind == OUT_F32) c = choose_config_tiled(M, N, K);  // fp32 partials: tiled kernel
   GemmArgs args;
   args.packed = static_cast<const uint8_t*>(packed->data);
   args.scales = static_cast<const uint16_t*>(scales);
@@ -1042,7 +1042,10 @@ tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* sca
     if (out_kind == OUT_F32) return launch_sk<true, OUT_F32>(A, args, c, s, ws);
     return bf16 ? launch_sk<true, OUT_ACT>(A, args, c, s, ws) : launch_sk<false, OUT_ACT>(A, args, c, s, ws);
   }
-  if (c.kind == 5) return bf16 ? launch_2sm<true>(A, args, s) : launch_2sm<false>(A, args, s);
+  if (c.kind == 5) {
+    if (out_kind == OUT_F32) return launch_2sm<true, OUT_F32>(A, args, s);
+    return bf16 ? launch_2sm<true, OUT_ACT>(A, args, s) : launch_2sm<false, OUT_ACT>(A, args, s);
+  }
   CUtensorMap map;
   st = act_tensor_map(A, M, a_K, c.NT, bf16, &map);
   if (st != TM_OK) return st;

@@ -45,7 +45,7 @@ struct Pair2Cfg {
   static constexpr int SMEM = 1024 + OFF_SZ + kSZSlots * 2 * kSZBox;
   static constexpr int TMEM_COLS = 512;           // accumulator 256 + 8 x 32 operand columns
   static_assert(NT + STAGES * 32 <= TMEM_COLS, "TMEM");
-  static_assert(ASTAGES * ACT_BYTES >= NT * kBN * 2, "C staging fits the drained activation ring");
+  static_assert(ASTAGES * ACT_BYTES >= NT * kBN * 4, "C staging (fp32) fits the drained activation ring");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
@@ -73,7 +73,8 @@ __device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst, const CUtensorMap*
       : "memory");
 }
 
-template <bool BF16>
+// OUT: OUT_ACT (bf16/fp16 C) or OUT_F32 (fp32 partials for the row-parallel TP reduce; bf16 A)
+template <bool BF16, int OUT>
 __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
     w4a16_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_c,
                           const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CUtensorMap tmap_z,
@@ -293,8 +294,9 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
     }
     if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % kSZSlots));
 
-    // epilogue: this CTA's accumulator (128 weight columns x 256 tokens) -> C tile [256][128];
-    // set d drains tokens [128 d, 128 d + 128)
+    // epilogue: this CTA's accumulator (128 weight columns x 256 tokens) -> C tile [256][128]
+    // staged in the drained activation ring; set d drains tokens [128 d, 128 d + 128)
+    constexpr int ES = OUT == OUT_F32 ? 4 : 2;
     mbar_wait(bar_acc, 0);
     tc_fence_after();
 #pragma unroll 1
@@ -304,9 +306,11 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
       tc_wait_ld();
 #pragma unroll
       for (int cc = 0; cc < 16; ++cc) {
-        uint8_t* dst = ring_ptr + (static_cast<size_t>(c0 + cc) * kBN + row) * 2;
+        uint8_t* dst = ring_ptr + (static_cast<size_t>(c0 + cc) * kBN + row) * ES;
         const float x = __uint_as_float(v[cc]);
-        if constexpr (BF16)
+        if constexpr (OUT == OUT_F32)
+          *reinterpret_cast<float*>(dst) = x;
+        else if constexpr (BF16)
           *reinterpret_cast<__nv_bfloat16*>(dst) = __float2bfloat16_rn(x);
         else
           *reinterpret_cast<__half*>(dst) = __float2half_rn(x);
@@ -315,7 +319,9 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
     fence_proxy_async_shared();
     asm volatile("bar.sync 1, 256;" ::: "memory");
     if (warp == 2 && lane == 0) {
-      tma_store_2d(&tmap_c, act0, nt * kBN, m0);
+      constexpr int ROWS = ES == 4 ? 128 : NT;  // the fp32 map's box is 128 rows (64 KB)
+      for (int r0 = 0; r0 < NT; r0 += ROWS)
+        if (m0 + r0 < args.M) tma_store_2d(&tmap_c, act0 + r0 * kBN * ES, nt * kBN, m0 + r0);
       bulk_commit_group();
       bulk_wait_group_read0();
     }

@@ -143,3 +143,26 @@ def test_deterministic():
     outs = [api.gemm_w4a16(t["A"], p, t["s"], t["z"]).clone() for _ in range(3)]
     torch.cuda.synchronize()
     assert all(torch.equal(outs[0], o) for o in outs[1:])
+
+
+@pytest.mark.parametrize("M", [700, 2049])
+def test_fp32_partials_oracle_and_tiled(M):
+    """fp32 partial output (row-parallel TP prefill): the 256 x 128 fp32 tile staged in the
+    activation ring and stored as two 128-row boxes (the second skipped past M); within the f32
+    bound of the oracle and bit-identical to the tiled kernel's partials."""
+    N, K, g = 2816, 1024, 128
+    d = synth.awq_like(M, N, K, group=g, seed=600 + M)
+    t = to_dev(d)
+    p = api.pack_w4(t["q"], t["s"], t["z"], g)
+    C = api.gemm_w4a16_partial_f32(t["A"], p, t["s"], t["z"])
+    api.set_prefill_pair(False)
+    try:
+        C_tiled = api.gemm_w4a16_partial_f32(t["A"], p, t["s"], t["z"])
+    finally:
+        api.set_prefill_pair(True)
+    torch.cuda.synchronize()
+    assert C.dtype == torch.float32 and torch.equal(C, C_tiled)
+    ref = gemm_f64(d["A"], d["q"], d["s"], d["z"], g)
+    r = compare.check(to_np64(C), ref, d["A"], d["q"], d["s"], d["z"], g, "f32")
+    _log(("pair", "f32", M), r)
+    assert r["ok"], compare.summary(r)
