@@ -359,7 +359,10 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
       else cnt = 128 * NDS + (FS ? 0 : 128);                 // szempty
       mbar_init(bar_fullw + 8 * b, cnt);
     }
-    if (push && lane == 0) mbar_init(bar_red, (CS - 1) * 128);
+    if (push && lane == 0) {  // one arrival (this one) + the ranks' st.async bytes
+      mbar_init(bar_red, 1);
+      mbar_arrive_expect_tx(bar_red, static_cast<uint32_t>((CS - 1) * 128 * NT * 4));
+    }
     fence_mbar_init();
     __syncwarp();
     if (lane == 0) {
@@ -410,16 +413,25 @@ __global__ void __launch_bounds__(DecCfg<NT, FS>::THREADS, 1)
       cluster_wait();  // pairs the setup arrive: the leader's bar_red is initialised
       cl_waited = true;
       if (rank > 0) {
-        const uint32_t dst = mapa_shared(red0 + ((rank - 1) * NT * 128 + row) * 4, 0);
+        // landing area [rank - 1][row][NT]: 4 x 16-byte st.async per thread, counted on the
+        // leader's bar_red (a release.cluster arrive here cost ~1000 cycles under HBM load)
+        const uint32_t dst = mapa_shared(red0 + ((rank - 1) * 128 + row) * NT * 4, 0);
+        const uint32_t rbar = mapa_shared(bar_red, 0);
 #pragma unroll
-        for (int m = 0; m < NT; ++m) st_cluster_f32(dst + m * 128 * 4, acc[m]);
-        mbar_arrive_remote(mapa_shared(bar_red, 0));  // release: this thread's pushes first
+        for (int m = 0; m < NT; m += 4) st_async_v4_f32(dst + m * 4, acc[m], acc[m + 1], acc[m + 2], acc[m + 3], rbar);
       } else {
         mbar_wait_cluster(bar_red, 0);
         const float* red = reinterpret_cast<const float*>(base_ptr + (red0 - base));
         for (int q = 1; q < CS; ++q) {  // rank order: deterministic
+          const float4* rq = reinterpret_cast<const float4*>(red + ((q - 1) * 128 + row) * NT);
 #pragma unroll
-          for (int m = 0; m < NT; ++m) acc[m] += red[(q - 1) * NT * 128 + m * 128 + row];
+          for (int m = 0; m < NT; m += 4) {
+            const float4 v = rq[m / 4];
+            acc[m] += v.x;
+            acc[m + 1] += v.y;
+            acc[m + 2] += v.z;
+            acc[m + 3] += v.w;
+          }
         }
 #pragma unroll
         for (int m = 0; m < NT; ++m)

@@ -451,7 +451,6 @@ __global__ void __launch_bounds__(RfCfg<NT, GROUP>::THREADS, RfCfg<NT, GROUP>::M
   // Warp cw owns columns 32 cw .. 32 cw + 31 of every tile (row groups 2 cw, 2 cw + 1) and reads
   // every chunk: no cross-warp reduction.  A segment = the CTA's consecutive chunks of one tile.
   const int cw = warp - 3;
-  constexpr float V = BF16 ? 128.0f : 1024.0f;
   // ldmatrix row address of this lane inside a blob: half (lane >> 4), row (lane & 15) of rg 2 cw
   const uint32_t lm_off =
       static_cast<uint32_t>((lane >> 4) * 2048 + (((lane >> 3) & 1) * 8 + (lane & 7)) * 16 + cw * 2 * 256);
