@@ -583,6 +583,38 @@ Config pk_config(int M, int N) {
   return c;
 }
 
+// clusters of `cs` pair-kernel CTAs that fit the GPU at once (one CTA per SM; clusters of 6-8
+// CTAs pack into the GPCs with leftovers, so fewer than SMs / cs -- a second wave of clusters
+// doubled the mid-M split-K time when this was not checked)
+int pair_active_clusters(int cs) {
+  static std::atomic<int> cache[kMaxDevices][9] = {};
+  const int dev = current_device();
+  if (cs < 2 || cs > 8) return 0;
+  int v = cache[dev][cs].load();
+  if (v > 0) return v;
+  auto kern = w4a16_gemm_2sm_kernel<true, OUT_ACT>;
+  static std::atomic<int> configured[kMaxDevices] = {};
+  const bool smem_ok = ensure_smem(kern, Pair2Cfg::SMEM, configured) == TM_OK;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cs * 32, 1, 1);
+  cfg.blockDim = dim3(Pair2Cfg::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = Pair2Cfg::SMEM;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (!smem_ok || cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+    (void)cudaGetLastError();
+    n = num_sms() / cs;  // (no device: the CPU-side query of the config)
+  }
+  cache[dev][cs].store(n);
+  return n;
+}
+
 // CTA-pair prefill kernel (gemm_2sm.cuh, kind 5): where the tiled chooser picks 256-token tiles
 // without split-K and N % 256 == 0 (bf16/fp16 outputs and fp32 partials).
 // Measured 4-9 % faster than the tiled kernel on every CFG#2 shape; on by
@@ -594,9 +626,26 @@ Config choose_config(int M, int N, int K) {
   if (use_rf(M)) return rf_config(M, N, K);
   if (use_pk(M)) return pk_config(M, N);
   Config c = choose_config_tiled(M, N, K);
-  if (g_pair.load() != 0 && c.kind == 0 && c.split == 1 && c.NT == Pair2Cfg::NT && N % 256 == 0 &&
-      g_override_tile.load() == 0 && g_override_split.load() == 0) {
+  if (g_pair.load() == 0 || N % 256 != 0 || g_override_tile.load() != 0 || g_override_split.load() != 0) return c;
+  if (c.kind == 0 && c.split == 1 && c.NT == Pair2Cfg::NT) {
     c.kind = 5;  // same grid: N / 128 CTAs (pairs along N) x M / 256
+  } else if (c.kind == 0 && M > 64 && M <= 512) {
+    // mid M: few 256-token pair tiles -> split K over up to 4 pairs of one cluster (2 S <= 8
+    // CTAs, reduced through distributed shared memory) while the clusters fit one wave
+    const int pairs = (N / 256) * ((M + Pair2Cfg::NT - 1) / Pair2Cfg::NT);
+    const int KS = K / 64;
+    int S = 1;
+    for (int k = 4; k >= 2; --k)
+      if (pairs <= pair_active_clusters(2 * k) && KS >= 4 * k) {
+        S = k;
+        break;
+      }
+    if (S == 1) return c;  // no split fits: the tiled kernel's smaller tiles (gate_up M = 128: 45 vs 55 us)
+    c.kind = 5;
+    c.NT = Pair2Cfg::NT;
+    c.split = S;
+    c.grid_x = (N / 128) * S;
+    c.grid_y = (M + Pair2Cfg::NT - 1) / Pair2Cfg::NT;
   }
   return c;
 }
@@ -865,13 +914,13 @@ tm_status launch_2sm(const void* A, const GemmArgs& args, cudaStream_t stream) {
   st = sz_tensor_map(args.zeros, args.K / args.group, args.N, &zmap);
   if (st != TM_OK) return st;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(args.N / 128, (args.M + Pair2Cfg::NT - 1) / Pair2Cfg::NT, 1);
+  cfg.gridDim = dim3(args.N / 128 * args.split, (args.M + Pair2Cfg::NT - 1) / Pair2Cfg::NT, 1);
   cfg.blockDim = dim3(Pair2Cfg::THREADS, 1, 1);
   cfg.dynamicSmemBytes = Pair2Cfg::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.x = 2 * args.split;  // S splits of one CTA pair
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
   attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -46,6 +46,9 @@ struct Pair2Cfg {
   static constexpr int TMEM_COLS = 512;           // accumulator 256 + 8 x 32 operand columns
   static_assert(NT + STAGES * 32 <= TMEM_COLS, "TMEM");
   static_assert(ASTAGES * ACT_BYTES >= NT * kBN * 4, "C staging (fp32) fits the drained activation ring");
+  // split-K: landing (S - 1 blocks of [128][slice + 4] fp32) + outgoing staging (S - 1 blocks) in
+  // the drained activation + weight + s/z rings (contiguous): <= 208 KB at S = 4
+  static_assert(ASTAGES * ACT_BYTES + STAGES * kBlobBytes + kSZSlots * 2 * kSZBox >= 2 * 3 * 128 * 68 * 4, "split-K");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
@@ -74,6 +77,14 @@ __device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst, const CUtensorMap*
 }
 
 // OUT: OUT_ACT (bf16/fp16 C) or OUT_F32 (fp32 partials for the row-parallel TP reduce; bf16 A)
+__device__ __forceinline__ void p2_stamp(const GemmArgs& a, int slot) {
+  if (a.trace && threadIdx.x == 64) {
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    a.trace[(blockIdx.y * gridDim.x + blockIdx.x) * kTraceSlots + slot] = static_cast<uint32_t>(gt);
+  }
+}
+
 template <bool BF16, int OUT>
 __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
     w4a16_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_c,
@@ -103,7 +114,9 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
   // outstanding tcgen05.commit (they returned only when the previous stage's MMAs completed,
   // serialising the tensor pipe; gemm_2sm trace)
   const uint32_t go_flags = tmem_slot + 8;
-  static_assert(8 * (6 * Cfg::STAGES + 2 * Cfg::ASTAGES + 2 * kSZSlots + 1) + 8 + 4 * Cfg::STAGES <= Cfg::HDR, "header");
+  // split-K (S > 1): the other splits' partials of this CTA's token slice land here (tx)
+  const uint32_t bar_land = go_flags + 4 * Cfg::STAGES;
+  static_assert(8 * (6 * Cfg::STAGES + 2 * Cfg::ASTAGES + 2 * kSZSlots + 2) + 8 + 4 * Cfg::STAGES <= Cfg::HDR, "header");
   const uint32_t act0 = base + Cfg::OFF_ACT, w0 = base + Cfg::OFF_W, sz0 = base + Cfg::OFF_SZ;
   const uint8_t* const w_ptr0 = base_ptr + Cfg::OFF_W;
   const uint8_t* const sz_ptr0 = base_ptr + Cfg::OFF_SZ;
@@ -111,18 +124,38 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
 
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();  // 0: leader
-  // banded raster over (n-tile pair, m-tile); CTA (2 j + rank) owns n-tile 2 j + rank
-  const int n_pairs = gridDim.x / 2, m_tiles = gridDim.y;
-  const int tile = blockIdx.y * n_pairs + static_cast<int>(blockIdx.x >> 1);
-  const int band = args.band;
-  const int b0 = (tile / (band * n_pairs)) * band;
-  const int rows = min(band, m_tiles - b0);
-  const int within = tile - b0 * n_pairs;
-  const int nt = 2 * (within / rows) + static_cast<int>(rank);
-  const int m0 = (b0 + within % rows) * NT;
-  const int KS = args.K / kBK;
+  // cluster of 2 S CTAs: rank = 2 sp + pr -- split sp (its K range) of pair member pr (pr = 0:
+  // the pair's leader, which issues the MMAs); S = 1 is one pair per cluster
+  const int S = args.split;
+  p2_stamp(args, 0);
+  const uint32_t rank = cluster_ctarank();
+  const uint32_t pr = rank & 1u, lead_rank = rank & ~1u;
+  const int sp = static_cast<int>(rank >> 1);
+  const uint16_t pair_mask = static_cast<uint16_t>(0x3u << lead_rank);  // multicast commits: the pair
+  int nt, m0;
+  if (S == 1) {
+    // banded raster over (n-tile pair, m-tile); CTA (2 j + pr) owns n-tile 2 j + pr
+    const int n_pairs = gridDim.x / 2, m_tiles = gridDim.y;
+    const int tile = blockIdx.y * n_pairs + static_cast<int>(blockIdx.x >> 1);
+    const int band = args.band;
+    const int b0 = (tile / (band * n_pairs)) * band;
+    const int rows = min(band, m_tiles - b0);
+    const int within = tile - b0 * n_pairs;
+    nt = 2 * (within / rows) + static_cast<int>(pr);
+    m0 = (b0 + within % rows) * NT;
+  } else {
+    nt = 2 * static_cast<int>(blockIdx.x / (2 * S)) + static_cast<int>(pr);
+    m0 = static_cast<int>(blockIdx.y) * NT;
+  }
+  const int KS_ALL = args.K / kBK;
+  const int ks0 = sp * KS_ALL / S;                 // this split's 64-k stages [ks0, ks0 + KS)
+  const int KS = (sp + 1) * KS_ALL / S - ks0;
+  // split-K token slices: split o finalises 16-token chunks [16 o / S, 16 (o + 1) / S) of the tile
+  const int own_lo = 16 * sp / S, own_hi = 16 * (sp + 1) / S;
   const int gshift = args.group == 64 ? 6 : 7;
+  // s/z boxes (8 groups each) of this split, ring slots and phases relative to its first box
+  const int box0 = ((ks0 * kBK) >> gshift) >> 3;
+
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmap_a);
@@ -144,6 +177,9 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
       mbar_init(bar_szempty + 8 * j, 256);  // both dequant sets
     }
     mbar_init(bar_acc, 1);
+    mbar_init(bar_land, 1);
+    if (S > 1)  // (S - 1) senders x one [128 columns][slice tokens + 4] fp32 block each
+      mbar_arrive_expect_tx(bar_land, static_cast<uint32_t>((S - 1) * 128 * (16 * (own_hi - own_lo) + 4) * 4));
     for (int s = 0; s < STAGES; ++s) st_shared_u32(go_flags + 4 * s, 0u);
     fence_mbar_init();
   }
@@ -165,19 +201,19 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ producer W: weights + s/z (local)
     if (lane == 0) {
-      const uint8_t* blob_g = args.packed + static_cast<size_t>(nt) * KS * kBlobBytes;
+      const uint8_t* blob_g = args.packed + (static_cast<size_t>(nt) * KS_ALL + ks0) * kBlobBytes;
       int box = -1;
       for (int i = 0; i < KS; ++i) {
         const int s = i % STAGES;
-        const int gb = ((i * kBK) >> gshift) >> 3;
-        if (gb != box) {
-          box = gb;
+        const int gb = (((ks0 + i) * kBK) >> gshift) >> 3;
+        if (gb - box0 != box) {
+          box = gb - box0;
           const int j = box % kSZSlots;
           mbar_wait(bar_szempty + 8 * j, ((box / kSZSlots) & 1) ^ 1);
           const uint32_t fb = bar_szfull + 8 * j;
           mbar_arrive_expect_tx(fb, 2 * kSZBox);
-          tma_load_2d(sz0 + j * 2 * kSZBox, &tmap_s, nt * kBN, 8 * box, fb);
-          tma_load_2d(sz0 + j * 2 * kSZBox + kSZBox, &tmap_z, nt * kBN, 8 * box, fb);
+          tma_load_2d(sz0 + j * 2 * kSZBox, &tmap_s, nt * kBN, 8 * gb, fb);
+          tma_load_2d(sz0 + j * 2 * kSZBox + kSZBox, &tmap_z, nt * kBN, 8 * gb, fb);
         }
         mbar_wait(bar_wempty + 8 * s, ((i / STAGES) & 1) ^ 1);
         const uint32_t fb = bar_wfull + 8 * s;
@@ -192,16 +228,17 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
       for (int i = 0; i < KS; ++i) {
         const int s = i % ASTAGES;
         mbar_wait(bar_aempty + 8 * s, ((i / ASTAGES) & 1) ^ 1);
-        if (rank == 0) mbar_arrive_expect_tx(bar_afull + 8 * s, 2 * Cfg::ACT_BYTES);  // both halves
-        const int aks = i >= args.a_ks ? i - args.a_ks : i;  // W8: low planes reuse A
-        tma_load_2d_2sm(act0 + s * Cfg::ACT_BYTES, &tmap_a, aks * kBK, m0 + static_cast<int>(rank) * HALF,
+        if (pr == 0) mbar_arrive_expect_tx(bar_afull + 8 * s, 2 * Cfg::ACT_BYTES);  // both halves
+        const int g = ks0 + i;
+        const int aks = g >= args.a_ks ? g - args.a_ks : g;  // W8: low planes reuse A
+        tma_load_2d_2sm(act0 + s * Cfg::ACT_BYTES, &tmap_a, aks * kBK, m0 + static_cast<int>(pr) * HALF,
                         bar_afull + 8 * s);
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader CTA only)
-    if (rank == 0 && lane == 0) {
+    if (pr == 0 && lane == 0) {
       constexpr uint32_t idesc = umma_idesc_f16(BF16, 256, NT);
       for (int i = 0; i < KS; ++i) {
         const int s = i % STAGES;
@@ -225,14 +262,14 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
 #pragma unroll
         for (int j = 0; j < kBK / 16; ++j)
           mma_ts_2sm(tmem_base, tmem_a0 + s * 32 + 8 * j, umma_desc_sw128(act + 32 * j), idesc, (i | j) != 0 ? 1u : 0u);
-        tc_commit_2sm(bar_empty + 8 * s, 0x3);  // both CTAs: TMEM operand slot (and act slot) free
+        tc_commit_2sm(bar_empty + 8 * s, pair_mask);  // both CTAs: TMEM operand slot (and act slot) free
       }
-      tc_commit_2sm(bar_acc, 0x3);
+      tc_commit_2sm(bar_acc, pair_mask);
     }
     __syncwarp();
   } else if (warp == 7) {
     // ------------------------------------------------------------ stage-ready relay (leader)
-    if (rank == 0 && lane == 0)
+    if (pr == 0 && lane == 0)
       for (int i = 0; i < KS; ++i) {
         const int s = i % STAGES;
         mbar_spin(bar_full + 8 * s, (i / STAGES) & 1);  // (peer arrivals do not wake a try_wait)
@@ -244,17 +281,20 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
     // two sets of 4 warps (2-5: even stages, 8-11: odd): one warp's dequant + TMEM store chain
     // is ~600 cycles per stage, above the 512-cycle MMA budget
     const int dset = warp >= 8 ? 1 : 0;
-    const bool lead = warp == 2 || warp == 10;  // relays activation-slot release
+    const bool relay = warp == 2 || warp == 10;  // relays activation-slot release
     const int quarter = warp & 3;
     const int row = quarter * 32 + static_cast<int>(lane);
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     int box = -1;
     for (int i = dset; i < KS; i += 2) {
       const int s = i % STAGES;
-      const int gl = (i * kBK) >> gshift;
-      if ((gl >> 3) != box) {
+      const int gl = ((ks0 + i) * kBK) >> gshift;
+      if ((gl >> 3) - box0 != box) {
         if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % kSZSlots));
-        box = gl >> 3;
+        // a box this set has no stage of (a split's first box can hold a single stage): release
+        // it too, or the producer would wait for its 256 arrivals when it reuses the slot
+        for (int k = box + 1; k < (gl >> 3) - box0; ++k) mbar_arrive(bar_szempty + 8 * (k % kSZSlots));
+        box = (gl >> 3) - box0;
         mbar_wait(bar_szfull + 8 * (box % kSZSlots), (box / kSZSlots) & 1);
       }
       mbar_wait(bar_wfull + 8 * s, (i / STAGES) & 1);
@@ -277,28 +317,146 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
       deq_word<BF16>(x1.z, s2, z2, r + 24);
       deq_word<BF16>(x1.w, s2, z2, r + 28);
       mbar_wait(bar_empty + 8 * s, ((i / STAGES) & 1) ^ 1);  // MMA(i - STAGES) done with the slot
-      if (lead && lane == 0 && i >= STAGES)  // relay: MMA(i - STAGES)'s activation slot is free
+      if (relay && lane == 0 && i >= STAGES)  // relay: MMA(i - STAGES)'s activation slot is free
         mbar_arrive(bar_aempty + 8 * ((i - STAGES) % ASTAGES));
       tc_fence_after();
       tmem_st_32x32b_x32(tmem_a0 + s * 32 + lane_off, r);
       tc_wait_st();
       tc_fence_before();
-      if (rank == 0) mbar_wait(bar_afull + 8 * (i % ASTAGES), (i / ASTAGES) & 1);  // both halves landed
+      if (pr == 0) mbar_wait(bar_afull + 8 * (i % ASTAGES), (i / ASTAGES) & 1);  // both halves landed
       __syncwarp();
       if (lane == 0) {  // the leader's barrier
-        if (rank == 0)
+        if (pr == 0)
           mbar_arrive(bar_full + 8 * s);
         else
-          mbar_arrive_remote_cta(mapa_shared(bar_full + 8 * s, 0));
+          mbar_arrive_remote_cta(mapa_shared(bar_full + 8 * s, lead_rank));
       }
     }
     if (box >= 0) mbar_arrive(bar_szempty + 8 * (box % kSZSlots));
 
-    // epilogue: this CTA's accumulator (128 weight columns x 256 tokens) -> C tile [256][128]
-    // staged in the drained activation ring; set d drains tokens [128 d, 128 d + 128)
     constexpr int ES = OUT == OUT_F32 ? 4 : 2;
     mbar_wait(bar_acc, 0);
     tc_fence_after();
+    p2_stamp(args, 1);
+    if (S > 1) {
+      // ---- split-K reduction over the cluster.  Every CTA of the cluster is past its MMAs
+      // (so its activation ring is drained) after this barrier; then each split sends its
+      // partial of every other split's token slice into that CTA's ring with st.async (16-byte
+      // vectors counted on its bar_land), and finalises its own slice: C = sum_s partial_s in
+      // split order (deterministic), stored straight from registers (row = weight column:
+      // 128 consecutive outputs per token, coalesced).  Landing layout at split o:
+      // [sender slot][column][slice tokens + 4 pad floats] (conflict-free 16-byte reads).
+      cluster_arrive();
+      cluster_wait();
+      p2_stamp(args, 2);
+      long long q0 = clock64(), q_ld = 0;
+      // stage this CTA's partials of the other slices in its own drained rings (after its
+      // landing area), each destination's block in the receiver's layout, then one bulk DSMEM
+      // copy per destination (scattered 16-byte st.async ran at ~2K cycles per chunk)
+      const uint32_t land_bytes = static_cast<uint32_t>((S - 1) * 128 * (16 * (own_hi - own_lo) + 4) * 4);
+      const auto out_off = [&](int o) {  // staging offset of destination o's block
+        uint32_t off = land_bytes;
+        for (int t = 0; t < o; ++t)
+          if (t != sp) off += static_cast<uint32_t>(128 * (16 * (16 * (t + 1) / S - 16 * t / S) + 4) * 4);
+        return off;
+      };
+      for (int c = dset; c < 16; c += 2) {
+        int o = 0;  // the chunk's owner: 16 o / S <= c < 16 (o + 1) / S (same bounds as own_lo/hi)
+        while (16 * (o + 1) / S <= c) ++o;
+        if (o == sp) continue;
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(tmem_base + lane_off + 16 * c, v);
+        tc_wait_ld();
+        const int o_lo = 16 * o / S, o_hi = 16 * (o + 1) / S;
+        const int stride = 16 * (o_hi - o_lo) + 4;
+        const uint32_t dst = act0 + out_off(o) + static_cast<uint32_t>((row * stride + 16 * (c - o_lo)) * 4);
+#pragma unroll
+        for (int q = 0; q < 16; q += 4)
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 4 * q), "r"(v[q]), "r"(v[q + 1]),
+                       "r"(v[q + 2]), "r"(v[q + 3])
+                       : "memory");
+      }
+      fence_proxy_async_shared();  // generic-proxy writes -> the bulk copy (async proxy)
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (threadIdx.x == 64) {
+        for (int o = 0; o < S; ++o) {
+          if (o == sp) continue;
+          const int stride = 16 * (16 * (o + 1) / S - 16 * o / S) + 4;
+          const uint32_t bytes = static_cast<uint32_t>(128 * stride * 4);
+          const uint32_t dst_rank = 2u * static_cast<uint32_t>(o) + pr;
+          const int slot = sp < o ? sp : sp - 1;
+          bulk_s2cluster(mapa_shared(act0 + static_cast<uint32_t>(slot) * bytes, dst_rank), act0 + out_off(o), bytes,
+                         mapa_shared(bar_land, dst_rank));
+        }
+      }
+      const long long q1 = clock64();
+      // one thread polls (256 spinning threads would compete with the incoming copies for the
+      // barrier unit), the other epilogue threads wait on a named barrier
+      if (threadIdx.x == 64) mbar_spin_cluster(bar_land, 0);  // (remote complete_tx does not wake a try_wait)
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      mbar_spin_cluster(bar_land, 0);  // (completed: orders this thread's reads after the bytes)
+      const long long q2 = clock64();
+      const int stride = 16 * (own_hi - own_lo) + 4;
+      const int n = nt * kBN + row;
+#pragma unroll 1
+      for (int c = own_lo; c < own_hi; ++c) {
+        if ((c & 1) != dset || m0 + 16 * c >= args.M) continue;
+        const long long q3 = clock64();
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(tmem_base + lane_off + 16 * c, v);
+        tc_wait_ld();
+        const long long q4 = clock64();
+        q_ld += q4 - q3;
+        // partials in split order: x = p_0 + p_1 + ... (own p_sp from TMEM, the others landed)
+        float x16[16];
+#pragma unroll
+        for (int cc = 0; cc < 16; ++cc) x16[cc] = 0.0f;
+        for (int t = 0; t < S; ++t) {
+          if (t == sp) {
+#pragma unroll
+            for (int cc = 0; cc < 16; ++cc) x16[cc] += __uint_as_float(v[cc]);
+          } else {
+            const uint32_t src =
+                act0 + static_cast<uint32_t>((((t < sp ? t : t - 1) * 128 + row) * stride + 16 * (c - own_lo)) * 4);
+#pragma unroll
+            for (int q = 0; q < 16; q += 4) {
+              float a0, a1, a2, a3;
+              asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                           : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3)
+                           : "r"(src + 4 * q));
+              x16[q] += a0;
+              x16[q + 1] += a1;
+              x16[q + 2] += a2;
+              x16[q + 3] += a3;
+            }
+          }
+        }
+#pragma unroll
+        for (int cc = 0; cc < 16; ++cc) {
+          const float x = x16[cc];
+          const int m = m0 + 16 * c + cc;
+          if (m < args.M) {
+            const size_t off = static_cast<size_t>(m) * args.N + n;
+            if constexpr (OUT == OUT_F32)
+              reinterpret_cast<float*>(args.out)[off] = x;
+            else if constexpr (BF16)
+              reinterpret_cast<__nv_bfloat16*>(args.out)[off] = __float2bfloat16_rn(x);
+            else
+              reinterpret_cast<__half*>(args.out)[off] = __float2half_rn(x);
+          }
+        }
+      }
+      if (args.trace && threadIdx.x == 64) {
+        const long long q5 = clock64();
+        uint32_t* tr = args.trace + (blockIdx.y * gridDim.x + blockIdx.x) * kTraceSlots;
+        tr[10] = static_cast<uint32_t>(q1 - q0);              // sends (TMEM loads + st.async)
+        tr[11] = static_cast<uint32_t>(q2 - q1);              // landing wait
+        tr[12] = static_cast<uint32_t>(q_ld);                 // own-slice TMEM loads
+        tr[13] = static_cast<uint32_t>(q5 - q2 - q_ld);       // own-slice sums + stores
+      }
+    } else {
+    // epilogue: this CTA's accumulator (128 weight columns x 256 tokens) -> C tile [256][128]
+    // staged in the drained activation ring; set d drains tokens [128 d, 128 d + 128)
 #pragma unroll 1
     for (int c0 = dset * (NT / 2); c0 < (dset + 1) * (NT / 2); c0 += 16) {
       uint32_t v[16];
@@ -325,7 +483,13 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
       bulk_commit_group();
       bulk_wait_group_read0();
     }
+    }
   }
+  if (S > 1 && !((warp >= 2 && warp < 6) || warp >= 8)) {
+    cluster_arrive();  // the split-K reduction's barrier (every thread of the cluster takes part)
+    cluster_wait();
+  }
+  p2_stamp(args, 5);
   grid_dependency_launch();
   tc_fence_before();
   __syncthreads();

@@ -166,3 +166,70 @@ def test_fp32_partials_oracle_and_tiled(M):
     r = compare.check(to_np64(C), ref, d["A"], d["q"], d["s"], d["z"], g, "f32")
     _log(("pair", "f32", M), r)
     assert r["ok"], compare.summary(r)
+
+
+# ---------------------------------------------------------------- split-K pairs (65 <= M <= 512)
+@pytest.mark.parametrize("M", [65, 128, 200, 256, 300, 512])
+@pytest.mark.parametrize("N,K,g", [(1024, 1216, 64), (1536, 2048, 128)])
+@pytest.mark.parametrize("act", ["bf16", "fp16"])
+def test_split_k_full_oracle(M, N, K, g, act):
+    """Mid M: S = 4 splits of one CTA pair per cluster (2 S = 8 CTAs), each split's K range
+    (K = 1216: 19 stages -> 4/5/5/5, s/z boxes straddling the split points at g = 64), the
+    token slices exchanged with st.async and summed in split order; ragged M (65, 200, 300:
+    chunks past M neither sent nor stored)."""
+    cfg = api.query_gemm_config(M, N, K)
+    assert cfg["kind"] == 5 and cfg["split_k"] > 1, cfg
+    d = synth.awq_like(M, N, K, group=g, seed=M * 7 + N + g, act_dtype=act)
+    C = _gemm(d, act)
+    ref = gemm_f64(d["A"], d["q"], d["s"], d["z"], g)
+    r = compare.check(to_np64(C), ref, d["A"], d["q"], d["s"], d["z"], g, act)
+    _log(("pair-split", M, N, K, act), r)
+    assert r["ok"], compare.summary(r)
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 6144, 4096), (128, 4096, 14336), (512, 4096, 4096), (100, 4096, 4096)])
+def test_split_k_cfg_shapes_sampled_rows(M, N, K):
+    cfg = api.query_gemm_config(M, N, K)
+    assert cfg["kind"] == 5 and cfg["split_k"] > 1, cfg
+    d = synth.awq_like_torch(M, N, K, seed=M + N + K)
+    p = api.pack_w4(d["q"], d["s"], d["z"], 128)
+    C = api.gemm_w4a16(d["A"], p, d["s"], d["z"])
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(M)
+    rows = sorted(set([0, M // 2, M - 1] + rng.integers(0, M, 9).tolist()))
+    A = d["A"].float().cpu().numpy()[rows]
+    q, s, z = (d[k].cpu().numpy() for k in ("q", "s", "z"))
+    ref = gemm_f64(A, q, s, z, 128)
+    r = compare.check(to_np64(C)[rows], ref, A, q, s, z, 128, "bf16")
+    _log(("pair-split-cfg", M, N, K), r)
+    assert r["ok"], compare.summary(r)
+
+
+def test_split_k_fp32_partials_and_determinism():
+    M, N, K, g = 256, 1536, 2048, 128
+    d = synth.awq_like(M, N, K, group=g, seed=31)
+    t = to_dev(d)
+    p = api.pack_w4(t["q"], t["s"], t["z"], g)
+    outs = [api.gemm_w4a16_partial_f32(t["A"], p, t["s"], t["z"]).clone() for _ in range(3)]
+    torch.cuda.synchronize()
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+    ref = gemm_f64(d["A"], d["q"], d["s"], d["z"], g)
+    r = compare.check(to_np64(outs[0]), ref, d["A"], d["q"], d["s"], d["z"], g, "f32")
+    _log(("pair-split", "f32"), r)
+    assert r["ok"], compare.summary(r)
+
+
+def test_split_k_w8_bit_planes():
+    M, N, K, g = 256, 2816, 2048, 128
+    assert api.query_gemm_config(M, N, 2 * K)["split_k"] > 1
+    rng = np.random.default_rng(23)
+    q8 = rng.integers(0, 256, size=(K, N), dtype=np.uint8)
+    z8 = rng.integers(0, 256, size=(K // g, N)).astype(np.float16)
+    s = (rng.uniform(0.5, 1.0, size=(K // g, N)) * 2.0 ** -10).astype(np.float16)
+    A = round_to(rng.standard_normal((M, K)), "bf16").astype(np.float32)
+    dev = "cuda"
+    p, s2, z2 = api.pack_w8(torch.from_numpy(q8).to(dev), torch.from_numpy(s).to(dev), torch.from_numpy(z8).to(dev), g)
+    C = api.gemm_w8a16(torch.from_numpy(A).to(dev).to(torch.bfloat16), p, s2, z2)
+    torch.cuda.synchronize()
+    W = (q8.astype(np.float64) - np.repeat(z8.astype(np.float64), g, axis=0)) * np.repeat(s.astype(np.float64), g, axis=0)
+    assert compare.relfro(to_np64(C), A.astype(np.float64) @ W) <= compare.RELFRO_TOL

@@ -31,23 +31,34 @@ def test_decode_configs_fit_one_wave(M, N, K):
 
 
 @pytest.mark.parametrize("M", [65, 100, 128, 200, 256, 300, 512])
-@pytest.mark.parametrize("N,K", SHAPES_8B + SHAPES_70B)
-def test_mid_m_cluster_split(M, N, K):
+@pytest.mark.parametrize("N,K", SHAPES_8B + SHAPES_70B + [(384, 4096), (640, 2048)])
+def test_mid_m_configs(M, N, K):
+    """65 <= M <= 512 with N % 256 == 0: CTA pairs (kind 5) with split-K over S pairs of one
+    cluster -- the largest S in 4..2 whose clusters of 2 S CTAs are co-resident for every pair
+    tile and leave >= 4 stages per split; with no such S the tiled kernel's configuration stays
+    (N % 256 != 0 too)."""
     c = api.query_gemm_config(M, N, K)
-    nt = c["tile_m"]
-    # 256-token tiles without a split run on CTA pairs (kind 5) when N % 256 == 0
-    assert c["kind"] == (5 if nt == 256 and c["split_k"] == 1 and N % 256 == 0 else 0)
-    if M <= 128:
-        assert nt == 128
-    elif M <= 256:
-        assert nt == (128 if 2 * (N // 128) <= SMS else 256)
-    else:
-        assert nt == 256
-    tiles = (N // 128) * ((M + nt - 1) // nt)
-    s = c["split_k"]
-    # the largest split in 2..4 that keeps tiles * split <= 128 CTAs, else no split
-    want = next((k for k in (4, 3, 2) if tiles * k <= 128), 1)
-    assert s == want, (tiles, s, want)
+    if N % 256 == 0:
+        # (the CPU-side query has no device: co-resident clusters of 2 S = SMS // (2 S))
+        pairs = (N // 256) * ((M + 255) // 256)
+        want = next((k for k in (4, 3, 2) if pairs <= SMS // (2 * k) and K // 64 >= 4 * k), 1)
+        if want > 1:
+            assert (c["kind"], c["tile_m"], c["split_k"]) == (5, 256, want), c
+            assert c["grid_ctas"] == (N // 128) * want * ((M + 255) // 256)
+            return
+        if c["kind"] == 5:  # the tiled chooser's own unsplit 256-token tiles run on pairs
+            assert c["split_k"] == 1 and c["tile_m"] == 256
+            return
+    assert c["kind"] == 0 and c["split_k"] >= 1  # the tiled kernel's cluster split (its caps apply)
+
+
+def test_mid_m_pair_toggle_restores_tiled_split():
+    api.set_prefill_pair(False)
+    try:
+        c = api.query_gemm_config(256, 4096, 4096)
+    finally:
+        api.set_prefill_pair(True)
+    assert c["kind"] == 0 and c["tile_m"] == 128
 
 
 @pytest.mark.parametrize("M", [1024, 2048, 4096, 8192])
