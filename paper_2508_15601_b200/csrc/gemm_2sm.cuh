@@ -19,6 +19,9 @@
 //  * one warp's dequant + TMEM store chain is ~600 cycles per stage -> two dequant sets;
 //  * activation loads see ~4000 cycles of latency under load -> an 11-slot activation ring,
 //    released by a dequant warp when it observes MMA(i - STAGES) done.
+// Mid M (args.split = S > 1): a cluster holds S pairs (rank = 2 split + pair member), split s
+// takes stages [s KS / S, (s + 1) KS / S), and the splits exchange partial token slices through
+// distributed shared memory (bulk copies) before each stores its slice.
 #pragma once
 #include <cstdint>
 #include <cuda.h>
@@ -76,7 +79,8 @@ __device__ __forceinline__ void tma_load_2d_2sm(uint32_t dst, const CUtensorMap*
       : "memory");
 }
 
-// OUT: OUT_ACT (bf16/fp16 C) or OUT_F32 (fp32 partials for the row-parallel TP reduce; bf16 A)
+// debug timeline (tm_set_trace): %globaltimer (ns, low 32 bits) of event `slot` of this CTA --
+// 0 start, 1 accumulator complete, 2 split-K cluster barrier, 3 partials sent, 4 landed, 5 end
 __device__ __forceinline__ void p2_stamp(const GemmArgs& a, int slot) {
   if (a.trace && threadIdx.x == 64) {
     uint64_t gt;
@@ -85,6 +89,7 @@ __device__ __forceinline__ void p2_stamp(const GemmArgs& a, int slot) {
   }
 }
 
+// OUT: OUT_ACT (bf16/fp16 C) or OUT_F32 (fp32 partials for the row-parallel TP reduce; bf16 A)
 template <bool BF16, int OUT>
 __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
     w4a16_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_c,
@@ -349,25 +354,27 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
       cluster_arrive();
       cluster_wait();
       p2_stamp(args, 2);
-      long long q0 = clock64(), q_ld = 0;
       // stage this CTA's partials of the other slices in its own drained rings (after its
       // landing area), each destination's block in the receiver's layout, then one bulk DSMEM
       // copy per destination (scattered 16-byte st.async ran at ~2K cycles per chunk)
+      // slice bounds bnd(k) = 16 k / S (k = 0..S; 16 past S) and staging offsets, computed once
+      // (integer divisions by the runtime S in the per-chunk loop cost ~1K cycles per chunk)
+      const int b1 = S > 1 ? 16 / S : 16, b2 = S > 2 ? 32 / S : 16, b3 = S > 3 ? 48 / S : 16;
+      const auto bnd = [&](int k) { return k <= 0 ? 0 : k == 1 ? b1 : k == 2 ? b2 : k == 3 ? b3 : 16; };
       const uint32_t land_bytes = static_cast<uint32_t>((S - 1) * 128 * (16 * (own_hi - own_lo) + 4) * 4);
-      const auto out_off = [&](int o) {  // staging offset of destination o's block
-        uint32_t off = land_bytes;
-        for (int t = 0; t < o; ++t)
-          if (t != sp) off += static_cast<uint32_t>(128 * (16 * (16 * (t + 1) / S - 16 * t / S) + 4) * 4);
-        return off;
-      };
+      const auto blk = [&](int o) { return static_cast<uint32_t>(128 * (16 * (bnd(o + 1) - bnd(o)) + 4) * 4); };
+      const uint32_t off1 = land_bytes + (sp != 0 ? blk(0) : 0u);
+      const uint32_t off2 = off1 + (sp != 1 ? blk(1) : 0u);
+      const uint32_t off3 = off2 + (sp != 2 ? blk(2) : 0u);
+      const auto out_off = [&](int o) { return o <= 0 ? land_bytes : o == 1 ? off1 : o == 2 ? off2 : off3; };
       for (int c = dset; c < 16; c += 2) {
-        int o = 0;  // the chunk's owner: 16 o / S <= c < 16 (o + 1) / S (same bounds as own_lo/hi)
-        while (16 * (o + 1) / S <= c) ++o;
+        // the chunk's owner: bnd(o) <= c < bnd(o + 1) (the same bounds as own_lo/hi)
+        const int o = (c >= b1 ? 1 : 0) + (c >= b2 ? 1 : 0) + (c >= b3 ? 1 : 0);
         if (o == sp) continue;
         uint32_t v[16];
         tmem_ld_32x32b_x16(tmem_base + lane_off + 16 * c, v);
         tc_wait_ld();
-        const int o_lo = 16 * o / S, o_hi = 16 * (o + 1) / S;
+        const int o_lo = bnd(o), o_hi = bnd(o + 1);
         const int stride = 16 * (o_hi - o_lo) + 4;
         const uint32_t dst = act0 + out_off(o) + static_cast<uint32_t>((row * stride + 16 * (c - o_lo)) * 4);
 #pragma unroll
@@ -381,32 +388,28 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
       if (threadIdx.x == 64) {
         for (int o = 0; o < S; ++o) {
           if (o == sp) continue;
-          const int stride = 16 * (16 * (o + 1) / S - 16 * o / S) + 4;
-          const uint32_t bytes = static_cast<uint32_t>(128 * stride * 4);
+          const uint32_t bytes = blk(o);
           const uint32_t dst_rank = 2u * static_cast<uint32_t>(o) + pr;
           const int slot = sp < o ? sp : sp - 1;
           bulk_s2cluster(mapa_shared(act0 + static_cast<uint32_t>(slot) * bytes, dst_rank), act0 + out_off(o), bytes,
                          mapa_shared(bar_land, dst_rank));
         }
       }
-      const long long q1 = clock64();
       // one thread polls (256 spinning threads would compete with the incoming copies for the
       // barrier unit), the other epilogue threads wait on a named barrier
+      p2_stamp(args, 3);
       if (threadIdx.x == 64) mbar_spin_cluster(bar_land, 0);  // (remote complete_tx does not wake a try_wait)
       asm volatile("bar.sync 1, 256;" ::: "memory");
       mbar_spin_cluster(bar_land, 0);  // (completed: orders this thread's reads after the bytes)
-      const long long q2 = clock64();
+      p2_stamp(args, 4);
       const int stride = 16 * (own_hi - own_lo) + 4;
       const int n = nt * kBN + row;
 #pragma unroll 1
       for (int c = own_lo; c < own_hi; ++c) {
         if ((c & 1) != dset || m0 + 16 * c >= args.M) continue;
-        const long long q3 = clock64();
         uint32_t v[16];
         tmem_ld_32x32b_x16(tmem_base + lane_off + 16 * c, v);
         tc_wait_ld();
-        const long long q4 = clock64();
-        q_ld += q4 - q3;
         // partials in split order: x = p_0 + p_1 + ... (own p_sp from TMEM, the others landed)
         float x16[16];
 #pragma unroll
@@ -445,14 +448,6 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
               reinterpret_cast<__half*>(args.out)[off] = __float2half_rn(x);
           }
         }
-      }
-      if (args.trace && threadIdx.x == 64) {
-        const long long q5 = clock64();
-        uint32_t* tr = args.trace + (blockIdx.y * gridDim.x + blockIdx.x) * kTraceSlots;
-        tr[10] = static_cast<uint32_t>(q1 - q0);              // sends (TMEM loads + st.async)
-        tr[11] = static_cast<uint32_t>(q2 - q1);              // landing wait
-        tr[12] = static_cast<uint32_t>(q_ld);                 // own-slice TMEM loads
-        tr[13] = static_cast<uint32_t>(q5 - q2 - q_ld);       // own-slice sums + stores
       }
     } else {
     // epilogue: this CTA's accumulator (128 weight columns x 256 tokens) -> C tile [256][128]

@@ -27,12 +27,8 @@ t = tr.cpu().numpy().astype(np.int64).reshape(G, 160)[:, :7] & 0xFFFFFFFF
 t0 = t[:, 0].min()
 rel = t - t0
 print("cfg", cfg)
-for k, name in enumerate(["start", "acc done", "cluster barrier", "(unused)", "(unused)", "end"]):
+for k, name in enumerate(["start", "acc done", "split-K cluster barrier", "sends issued", "landed", "end"]):
     col = rel[:, k]
     col = col[t[:, k] != 0]
     if len(col):
         print(f"  {name:16s} median {np.median(col):9.0f} ns  min {col.min():9.0f}  max {col.max():9.0f}")
-ph = tr.cpu().numpy().astype(np.int64).reshape(G, 160)[:, 10:14]
-if ph.any():
-    for k, name in enumerate(["sends (cyc)", "landing wait", "own TMEM loads", "own sums+stores"]):
-        print(f"  {name:16s} median {np.median(ph[:, k]):9.0f} cycles  max {ph[:, k].max():9.0f}")
