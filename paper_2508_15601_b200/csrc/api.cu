@@ -586,19 +586,20 @@ Config pk_config(int M, int N) {
 // clusters of `cs` pair-kernel CTAs that fit the GPU at once (one CTA per SM; clusters of 6-8
 // CTAs pack into the GPCs with leftovers, so fewer than SMs / cs -- a second wave of clusters
 // doubled the mid-M split-K time when this was not checked)
+template <int NT>
 int pair_active_clusters(int cs) {
   static std::atomic<int> cache[kMaxDevices][9] = {};
   const int dev = current_device();
   if (cs < 2 || cs > 8) return 0;
   int v = cache[dev][cs].load();
   if (v > 0) return v;
-  auto kern = w4a16_gemm_2sm_kernel<true, OUT_ACT>;
+  auto kern = w4a16_gemm_2sm_kernel<NT, true, OUT_ACT>;
   static std::atomic<int> configured[kMaxDevices] = {};
-  const bool smem_ok = ensure_smem(kern, Pair2Cfg::SMEM, configured) == TM_OK;
+  const bool smem_ok = ensure_smem(kern, PairCfg<NT>::SMEM, configured) == TM_OK;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(cs * 32, 1, 1);
-  cfg.blockDim = dim3(Pair2Cfg::THREADS, 1, 1);
-  cfg.dynamicSmemBytes = Pair2Cfg::SMEM;
+  cfg.blockDim = dim3(PairCfg<NT>::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = PairCfg<NT>::SMEM;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = cs;
@@ -636,7 +637,7 @@ Config choose_config(int M, int N, int K) {
     const int KS = K / 64;
     int S = 1;
     for (int k = 4; k >= 2; --k)
-      if (pairs <= pair_active_clusters(2 * k) && KS >= 4 * k) {
+      if (pairs <= pair_active_clusters<256>(2 * k) && KS >= 4 * k) {
         S = k;
         break;
       }
@@ -646,6 +647,22 @@ Config choose_config(int M, int N, int K) {
     c.split = S;
     c.grid_x = (N / 128) * S;
     c.grid_y = (M + Pair2Cfg::NT - 1) / Pair2Cfg::NT;
+  } else if (g_pair.load() >= 2 && (c.kind == 1 || c.kind == 2) && M > 16 && M <= 64) {
+    // small M on 64-token pair tiles (M = 256 x N = 64 MMAs), split K over up to 4 pairs
+    const int pairs = N / 256;
+    const int KS = K / 64;
+    int S = 1;
+    for (int k = 4; k >= 2; --k)
+      if (pairs <= pair_active_clusters<64>(2 * k) && KS >= 4 * k) {
+        S = k;
+        break;
+      }
+    if (S == 1) return c;
+    c.kind = 5;
+    c.NT = 64;
+    c.split = S;
+    c.grid_x = (N / 128) * S;
+    c.grid_y = 1;
   }
   return c;
 }
@@ -898,25 +915,26 @@ tm_status launch_gemm(const CUtensorMap& map, const GemmArgs& args, const Config
 
 // CTA-pair prefill (gemm_2sm.cuh): where the tiled kernel would run 128 x 256 tiles without
 // split-K, N % 256 == 0, bf16/fp16 output.
-template <bool BF16, int OUT>
-tm_status launch_2sm(const void* A, const GemmArgs& args, cudaStream_t stream) {
-  auto kern = w4a16_gemm_2sm_kernel<BF16, OUT>;
+template <int NT, bool BF16, int OUT>
+tm_status launch_2sm_t(const void* A, const GemmArgs& args, cudaStream_t stream) {
+  using Cfg = PairCfg<NT>;
+  auto kern = w4a16_gemm_2sm_kernel<NT, BF16, OUT>;
   static std::atomic<int> configured[kMaxDevices] = {};
-  tm_status st = ensure_smem(kern, Pair2Cfg::SMEM, configured);
+  tm_status st = ensure_smem(kern, Cfg::SMEM, configured);
   if (st != TM_OK) return st;
   CUtensorMap amap, cmap, smap, zmap;
-  st = act_tensor_map(A, args.M, args.a_ks * 64, Pair2Cfg::HALF, BF16, &amap);
+  st = act_tensor_map(A, args.M, args.a_ks * 64, Cfg::HALF, BF16, &amap);
   if (st != TM_OK) return st;
-  st = out_tensor_map(args.out, args.M, args.N, Pair2Cfg::NT, OUT == OUT_F32 ? 4 : 2, BF16, &cmap);
+  st = out_tensor_map(args.out, args.M, args.N, Cfg::NT, OUT == OUT_F32 ? 4 : 2, BF16, &cmap);
   if (st != TM_OK) return st;
   st = sz_tensor_map(args.scales, args.K / args.group, args.N, &smap);
   if (st != TM_OK) return st;
   st = sz_tensor_map(args.zeros, args.K / args.group, args.N, &zmap);
   if (st != TM_OK) return st;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(args.N / 128 * args.split, (args.M + Pair2Cfg::NT - 1) / Pair2Cfg::NT, 1);
-  cfg.blockDim = dim3(Pair2Cfg::THREADS, 1, 1);
-  cfg.dynamicSmemBytes = Pair2Cfg::SMEM;
+  cfg.gridDim = dim3(args.N / 128 * args.split, (args.M + Cfg::NT - 1) / Cfg::NT, 1);
+  cfg.blockDim = dim3(Cfg::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = stream;
   cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
@@ -932,6 +950,11 @@ tm_status launch_2sm(const void* A, const GemmArgs& args, cudaStream_t stream) {
     return TM_ERR_CUDA;
   }
   return TM_OK;
+}
+
+template <bool BF16, int OUT>
+tm_status launch_2sm(const void* A, const GemmArgs& args, int nt, cudaStream_t stream) {
+  return nt == 64 ? launch_2sm_t<64, BF16, OUT>(A, args, stream) : launch_2sm_t<256, BF16, OUT>(A, args, stream);
 }
 
 template <bool BF16>
@@ -1092,8 +1115,8 @@ tm_status gemm_common(const void* A, const tm_packed_w4* packed, const void* sca
     return bf16 ? launch_sk<true, OUT_ACT>(A, args, c, s, ws) : launch_sk<false, OUT_ACT>(A, args, c, s, ws);
   }
   if (c.kind == 5) {
-    if (out_kind == OUT_F32) return launch_2sm<true, OUT_F32>(A, args, s);
-    return bf16 ? launch_2sm<true, OUT_ACT>(A, args, s) : launch_2sm<false, OUT_ACT>(A, args, s);
+    if (out_kind == OUT_F32) return launch_2sm<true, OUT_F32>(A, args, c.NT, s);
+    return bf16 ? launch_2sm<true, OUT_ACT>(A, args, c.NT, s) : launch_2sm<false, OUT_ACT>(A, args, c.NT, s);
   }
   CUtensorMap map;
   st = act_tensor_map(A, M, a_K, c.NT, bf16, &map);
@@ -1530,7 +1553,8 @@ tm_status tm_set_prefill_persistent(int on) {
 }
 
 tm_status tm_set_prefill_pair(int on) {
-  g_pair.store(on ? 1 : 0);
+  if (on < 0 || on > 2) return TM_ERR_INVALID_ARG;
+  g_pair.store(on);
   return TM_OK;
 }
 

@@ -34,26 +34,31 @@
 
 namespace w4k {
 
-struct Pair2Cfg {
-  static constexpr int NT = 256;                  // tokens per pair tile (N of the MMA)
+template <int NT_>
+struct PairCfg {
+  static constexpr int NT = NT_;                  // tokens per pair tile (N of the MMA): 256 or 64
   static constexpr int HALF = NT / 2;             // tokens staged per CTA
   static constexpr int STAGES = 8;    // weight + TMEM operand slots (a multiple of 4: go-flag groups)
   static constexpr int ASTAGES = 11;  // activation slots (L2 latency under load ~4000 cycles)
   static constexpr int THREADS = 384;
-  static constexpr int ACT_BYTES = HALF * 128;    // 16 KB: 128 tokens x 64 k (SW128)
+  static constexpr int ACT_BYTES = HALF * 128;    // 16 KB (NT = 256): 128 tokens x 64 k (SW128)
   static constexpr int HDR = 1024;
   static constexpr int OFF_ACT = HDR;
   static constexpr int OFF_W = OFF_ACT + ASTAGES * ACT_BYTES;
   static constexpr int OFF_SZ = OFF_W + STAGES * kBlobBytes;
-  static constexpr int SMEM = 1024 + OFF_SZ + kSZSlots * 2 * kSZBox;
-  static constexpr int TMEM_COLS = 512;           // accumulator 256 + 8 x 32 operand columns
+  static constexpr int SMEM_USED = 1024 + OFF_SZ + kSZSlots * 2 * kSZBox;
+  // one CTA per SM: each allocates all 512 TMEM columns (NT = 64 pads its request past half)
+  static constexpr int SMEM = SMEM_USED > 117 * 1024 ? SMEM_USED : 117 * 1024;
+  static constexpr int TMEM_COLS = 512;           // accumulator NT + 8 x 32 operand columns
   static_assert(NT + STAGES * 32 <= TMEM_COLS, "TMEM");
   static_assert(ASTAGES * ACT_BYTES >= NT * kBN * 4, "C staging (fp32) fits the drained activation ring");
   // split-K: landing (S - 1 blocks of [128][slice + 4] fp32) + outgoing staging (S - 1 blocks) in
-  // the drained activation + weight + s/z rings (contiguous): <= 208 KB at S = 4
-  static_assert(ASTAGES * ACT_BYTES + STAGES * kBlobBytes + kSZSlots * 2 * kSZBox >= 2 * 3 * 128 * 68 * 4, "split-K");
+  // the drained activation + weight + s/z rings (contiguous): <= 208 KB at NT = 256, S = 4
+  static_assert(ASTAGES * ACT_BYTES + STAGES * kBlobBytes + kSZSlots * 2 * kSZBox >= 2 * 3 * 128 * (NT / 4 + 4) * 4,
+                "split-K");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
+using Pair2Cfg = PairCfg<256>;
 
 __device__ __forceinline__ void mma_ts_2sm(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                            uint32_t accumulate) {
@@ -90,13 +95,14 @@ __device__ __forceinline__ void p2_stamp(const GemmArgs& a, int slot) {
 }
 
 // OUT: OUT_ACT (bf16/fp16 C) or OUT_F32 (fp32 partials for the row-parallel TP reduce; bf16 A)
-template <bool BF16, int OUT>
-__global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
+template <int NT_, bool BF16, int OUT>
+__global__ void __launch_bounds__(PairCfg<NT_>::THREADS, 1)
     w4a16_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_c,
                           const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CUtensorMap tmap_z,
                           const GemmArgs args) {
-  using Cfg = Pair2Cfg;
+  using Cfg = PairCfg<NT_>;
   constexpr int NT = Cfg::NT, HALF = Cfg::HALF, STAGES = Cfg::STAGES, ASTAGES = Cfg::ASTAGES;
+  constexpr int NCH = NT / 16;  // 16-token chunks of a tile (split-K token slices)
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* const base_ptr = smem_raw + (base - smem_u32(smem_raw));
@@ -156,7 +162,7 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
   const int ks0 = sp * KS_ALL / S;                 // this split's 64-k stages [ks0, ks0 + KS)
   const int KS = (sp + 1) * KS_ALL / S - ks0;
   // split-K token slices: split o finalises 16-token chunks [16 o / S, 16 (o + 1) / S) of the tile
-  const int own_lo = 16 * sp / S, own_hi = 16 * (sp + 1) / S;
+  const int own_lo = NCH * sp / S, own_hi = NCH * (sp + 1) / S;
   const int gshift = args.group == 64 ? 6 : 7;
   // s/z boxes (8 groups each) of this split, ring slots and phases relative to its first box
   const int box0 = ((ks0 * kBK) >> gshift) >> 3;
@@ -359,15 +365,15 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
       // copy per destination (scattered 16-byte st.async ran at ~2K cycles per chunk)
       // slice bounds bnd(k) = 16 k / S (k = 0..S; 16 past S) and staging offsets, computed once
       // (integer divisions by the runtime S in the per-chunk loop cost ~1K cycles per chunk)
-      const int b1 = S > 1 ? 16 / S : 16, b2 = S > 2 ? 32 / S : 16, b3 = S > 3 ? 48 / S : 16;
-      const auto bnd = [&](int k) { return k <= 0 ? 0 : k == 1 ? b1 : k == 2 ? b2 : k == 3 ? b3 : 16; };
+      const int b1 = S > 1 ? NCH / S : NCH, b2 = S > 2 ? 2 * NCH / S : NCH, b3 = S > 3 ? 3 * NCH / S : NCH;
+      const auto bnd = [&](int k) { return k <= 0 ? 0 : k == 1 ? b1 : k == 2 ? b2 : k == 3 ? b3 : NCH; };
       const uint32_t land_bytes = static_cast<uint32_t>((S - 1) * 128 * (16 * (own_hi - own_lo) + 4) * 4);
       const auto blk = [&](int o) { return static_cast<uint32_t>(128 * (16 * (bnd(o + 1) - bnd(o)) + 4) * 4); };
       const uint32_t off1 = land_bytes + (sp != 0 ? blk(0) : 0u);
       const uint32_t off2 = off1 + (sp != 1 ? blk(1) : 0u);
       const uint32_t off3 = off2 + (sp != 2 ? blk(2) : 0u);
       const auto out_off = [&](int o) { return o <= 0 ? land_bytes : o == 1 ? off1 : o == 2 ? off2 : off3; };
-      for (int c = dset; c < 16; c += 2) {
+      for (int c = dset; c < NCH; c += 2) {
         // the chunk's owner: bnd(o) <= c < bnd(o + 1) (the same bounds as own_lo/hi)
         const int o = (c >= b1 ? 1 : 0) + (c >= b2 ? 1 : 0) + (c >= b3 ? 1 : 0);
         if (o == sp) continue;
@@ -472,7 +478,7 @@ __global__ void __launch_bounds__(Pair2Cfg::THREADS, 1)
     fence_proxy_async_shared();
     asm volatile("bar.sync 1, 256;" ::: "memory");
     if (warp == 2 && lane == 0) {
-      constexpr int ROWS = ES == 4 ? 128 : NT;  // the fp32 map's box is 128 rows (64 KB)
+      constexpr int ROWS = ES == 4 && NT > 128 ? 128 : NT;  // the fp32 map's box is <= 128 rows
       for (int r0 = 0; r0 < NT; r0 += ROWS)
         if (m0 + r0 < args.M) tma_store_2d(&tmap_c, act0 + r0 * kBN * ES, nt * kBN, m0 + r0);
       bulk_commit_group();

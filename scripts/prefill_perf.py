@@ -37,7 +37,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--ms", default="2048,4096,8192")
 ap.add_argument("--shapes", default="qkv,o,gate_up,down")
 ap.add_argument("--ab", action="store_true")
+ap.add_argument("--pair-mode", type=int, default=1)
 a = ap.parse_args()
+api.set_prefill_pair(a.pair_mode)
 for name in a.shapes.split(","):
     N, K = SHAPES[name]
     d = synth.awq_like_torch(1, N, K, seed=3)
@@ -54,7 +56,7 @@ for name in a.shapes.split(","):
         if a.ab:
             api.set_prefill_pair(False)
             tt = gtime(lambda: api.gemm_w4a16(A, p, d["s"], d["z"], out=C))
-            api.set_prefill_pair(True)
+            api.set_prefill_pair(a.pair_mode)
             extra = f"   tiled {tt:8.1f} us ratio {td / tt:5.2f}"
         print(f"  {name:8s} M={M:5d}  w4a16(kind {kind}) {t:8.1f} us {fl / t / 1e6:7.1f} TF/s   torch bf16 {td:8.1f} us "
               f"{fl / td / 1e6:7.1f} TF/s   ratio {td / t:5.2f}{extra}", flush=True)

@@ -233,3 +233,28 @@ def test_split_k_w8_bit_planes():
     torch.cuda.synchronize()
     W = (q8.astype(np.float64) - np.repeat(z8.astype(np.float64), g, axis=0)) * np.repeat(s.astype(np.float64), g, axis=0)
     assert compare.relfro(to_np64(C), A.astype(np.float64) @ W) <= compare.RELFRO_TOL
+
+
+# ---------------------------------------------------------------- 64-token pair tiles (opt-in)
+@pytest.mark.parametrize("M,N,K,g", [(64, 1024, 1216, 64), (17, 2816, 2048, 128), (40, 1536, 2048, 128)])
+@pytest.mark.parametrize("act", ["bf16", "fp16"])
+def test_pair64_opt_in_full_oracle(M, N, K, g, act):
+    """tm_set_prefill_pair(2): 17 <= M <= 64 on 64-token pair tiles (M = 256 x N = 64 MMAs, each
+    CTA staging 32 tokens), split-K over the cluster with 16-token slices (4 chunks per tile)."""
+    api.set_prefill_pair(2)
+    try:
+        cfg = api.query_gemm_config(M, N, K)
+        assert cfg["kind"] == 5 and cfg["tile_m"] == 64 and cfg["split_k"] > 1, cfg
+        d = synth.awq_like(M, N, K, group=g, seed=M * 3 + N + g, act_dtype=act)
+        C = _gemm(d, act)
+    finally:
+        api.set_prefill_pair(True)
+    ref = gemm_f64(d["A"], d["q"], d["s"], d["z"], g)
+    r = compare.check(to_np64(C), ref, d["A"], d["q"], d["s"], d["z"], g, act)
+    _log(("pair64", M, N, K, act), r)
+    assert r["ok"], compare.summary(r)
+
+
+def test_set_prefill_pair_rejects_bad_mode():
+    with pytest.raises(api.TMError):
+        api.set_prefill_pair(3)
