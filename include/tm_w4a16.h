@@ -137,9 +137,14 @@ tm_status tm_gemm_w8a16(const void* A, const tm_packed_w4* packed, const void* s
  *             rounding.  K is split over a thread-block cluster reduced in distributed shared
  *             memory when the tiles are few, else over a persistent stream-K grid whose
  *             shared tiles are reduced through the workspace (fixed order: deterministic).
- *   M > 64  : tiled (prefill) kernel, reading R6: weights rounded once to bf16,
- *             RNE_bf16((q - z) * RNE_bf16(s)), before the MMA; for 65 <= M <= 512 K may be
- *             split over a cluster (DSMEM reduction).
+ *   M > 64  : prefill kernels, reading R6: weights rounded once to bf16,
+ *             RNE_bf16((q - z) * RNE_bf16(s)), before the MMA.  N % 256 == 0: CTA pairs
+ *             (tcgen05 cta_group::2; 256 weight columns x 256 tokens per pair) -- unsplit
+ *             where the tiles fill the GPU, for 65 <= M <= 512 K split over up to 4 pairs of
+ *             one cluster (partials exchanged by bulk DSMEM copies, summed in split order).
+ *             Otherwise the single-CTA tiled kernel (128 columns x 128/256 tokens; for
+ *             65 <= M <= 512 K may be split over a cluster, DSMEM reduction).  Both prefill
+ *             kernels take the same MMA order along K: identical results where both apply.
  * Results are deterministic run to run.  Uses the library-owned workspace (see above).    */
 tm_status tm_gemm_w4a16(const void* A, const tm_packed_w4* packed,
                         const void* scales, const void* zeros, void* C,
