@@ -143,8 +143,9 @@ tm_status tm_gemm_w8a16(const void* A, const tm_packed_w4* packed, const void* s
  *             where the tiles fill the GPU, for 65 <= M <= 512 K split over up to 4 pairs of
  *             one cluster (partials exchanged by bulk DSMEM copies, summed in split order).
  *             Otherwise the single-CTA tiled kernel (128 columns x 128/256 tokens; for
- *             65 <= M <= 512 K may be split over a cluster, DSMEM reduction).  Both prefill
- *             kernels take the same MMA order along K: identical results where both apply.
+ *             65 <= M <= 512 K may be split over a cluster, DSMEM reduction).  Unsplit, the
+ *             two prefill kernels take the same MMA order along K (identical results); a
+ *             split changes only the fp32 summation order of the per-split partials.
  * Results are deterministic run to run.  Uses the library-owned workspace (see above).    */
 tm_status tm_gemm_w4a16(const void* A, const tm_packed_w4* packed,
                         const void* scales, const void* zeros, void* C,
