@@ -47,7 +47,8 @@ tm_status tm_set_prefill_persistent(int on);
  * the tiled kernel would run 256-token tiles without split-K and N % 256 == 0 (bf16/fp16
  * outputs and fp32 partials).  on = 0 restores the tiled kernel (kind 0)
  * there -- A/B measurements and tests; on = 2 additionally runs 17 <= M <= 64 on 64-token
- * pair tiles with split-K (experiment).  Default 1; other values: TM_ERR_INVALID_ARG.      */
+ * pair tiles with split-K (experiment); on = 3 is 1 with 256-token instead of 128-token pair
+ * tiles at 65 <= M <= 128 (A/B).  Default 1; other values: TM_ERR_INVALID_ARG.             */
 tm_status tm_set_prefill_pair(int on);
 
 /* Decode cluster mode: 0 automatic (default), 1 never (always stream-K), 2..8 force that many

@@ -395,7 +395,8 @@ def set_prefill_persistent(on=True):
 
 def set_prefill_pair(on=True):
     """Tests/benchmarks: CTA-pair prefill kernel (kind 5, the default where it applies) on/off;
-    on=2 also runs 17 <= M <= 64 on 64-token pair tiles (experiment)."""
+    on=2 also runs 17 <= M <= 64 on 64-token pair tiles (experiment); on=3 keeps 256-token tiles at
+    M <= 128 (A/B)."""
     _check(lib().tm_set_prefill_pair(int(on) if not isinstance(on, bool) else (1 if on else 0)))
 
 

@@ -621,6 +621,7 @@ int pair_active_clusters(int cs) {
 // Measured 4-9 % faster than the tiled kernel on every CFG#2 shape; on by
 // default, tm_set_prefill_pair(0) restores the tiled kernel (A/B, tests).
 std::atomic<int> g_pair{1};
+std::atomic<int> g_pair128{1};  // (A/B: tm_set_prefill_pair(3) = 256-token tiles for M <= 128 too)
 
 Config choose_config_tiled(int M, int N, int K);
 Config choose_config(int M, int N, int K) {
@@ -631,22 +632,26 @@ Config choose_config(int M, int N, int K) {
   if (c.kind == 0 && c.split == 1 && c.NT == Pair2Cfg::NT) {
     c.kind = 5;  // same grid: N / 128 CTAs (pairs along N) x M / 256
   } else if (c.kind == 0 && M > 64 && M <= 512) {
-    // mid M: few 256-token pair tiles -> split K over up to 4 pairs of one cluster (2 S <= 8
-    // CTAs, reduced through distributed shared memory) while the clusters fit one wave
-    const int pairs = (N / 256) * ((M + Pair2Cfg::NT - 1) / Pair2Cfg::NT);
+    // mid M: few pair tiles -> split K over up to 4 pairs of one cluster (2 S <= 8 CTAs,
+    // reduced through distributed shared memory) while the clusters fit one wave; M <= 128 on
+    // 128-token pair tiles (half the MMA work of a 256-token tile)
+    const int ntile = (M <= 128 && g_pair128.load() != 0) ? 128 : 256;
+    const int pairs = (N / 256) * ((M + ntile - 1) / ntile);
     const int KS = K / 64;
     int S = 1;
-    for (int k = 4; k >= 2; --k)
-      if (pairs <= pair_active_clusters<256>(2 * k) && KS >= 4 * k) {
+    for (int k = 4; k >= 2; --k) {
+      const int act = ntile == 128 ? pair_active_clusters<128>(2 * k) : pair_active_clusters<256>(2 * k);
+      if (pairs <= act && KS >= 4 * k) {
         S = k;
         break;
       }
+    }
     if (S == 1) return c;  // no split fits: the tiled kernel's smaller tiles (gate_up M = 128: 45 vs 55 us)
     c.kind = 5;
-    c.NT = Pair2Cfg::NT;
+    c.NT = ntile;
     c.split = S;
     c.grid_x = (N / 128) * S;
-    c.grid_y = (M + Pair2Cfg::NT - 1) / Pair2Cfg::NT;
+    c.grid_y = (M + ntile - 1) / ntile;
   } else if (g_pair.load() >= 2 && (c.kind == 1 || c.kind == 2) && M > 16 && M <= 64) {
     // small M on 64-token pair tiles (M = 256 x N = 64 MMAs), split K over up to 4 pairs
     const int pairs = N / 256;
@@ -954,7 +959,9 @@ tm_status launch_2sm_t(const void* A, const GemmArgs& args, cudaStream_t stream)
 
 template <bool BF16, int OUT>
 tm_status launch_2sm(const void* A, const GemmArgs& args, int nt, cudaStream_t stream) {
-  return nt == 64 ? launch_2sm_t<64, BF16, OUT>(A, args, stream) : launch_2sm_t<256, BF16, OUT>(A, args, stream);
+  if (nt == 64) return launch_2sm_t<64, BF16, OUT>(A, args, stream);
+  if (nt == 128) return launch_2sm_t<128, BF16, OUT>(A, args, stream);
+  return launch_2sm_t<256, BF16, OUT>(A, args, stream);
 }
 
 template <bool BF16>
@@ -1553,8 +1560,9 @@ tm_status tm_set_prefill_persistent(int on) {
 }
 
 tm_status tm_set_prefill_pair(int on) {
-  if (on < 0 || on > 2) return TM_ERR_INVALID_ARG;
-  g_pair.store(on);
+  if (on < 0 || on > 3) return TM_ERR_INVALID_ARG;
+  g_pair.store(on == 3 ? 1 : on);
+  g_pair128.store(on == 3 ? 0 : 1);
   return TM_OK;
 }
 

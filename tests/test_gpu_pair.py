@@ -257,4 +257,14 @@ def test_pair64_opt_in_full_oracle(M, N, K, g, act):
 
 def test_set_prefill_pair_rejects_bad_mode():
     with pytest.raises(api.TMError):
-        api.set_prefill_pair(3)
+        api.set_prefill_pair(4)
+
+
+def test_mid_m_128_token_tiles_and_mode3():
+    """M <= 128 runs 128-token pair tiles (default); mode 3 keeps 256-token tiles there (A/B)."""
+    assert api.query_gemm_config(128, 4096, 4096)["tile_m"] == 128
+    api.set_prefill_pair(3)
+    try:
+        assert api.query_gemm_config(128, 4096, 4096)["tile_m"] == 256
+    finally:
+        api.set_prefill_pair(True)

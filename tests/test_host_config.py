@@ -40,11 +40,12 @@ def test_mid_m_configs(M, N, K):
     c = api.query_gemm_config(M, N, K)
     if N % 256 == 0:
         # (the CPU-side query has no device: co-resident clusters of 2 S = SMS // (2 S))
-        pairs = (N // 256) * ((M + 255) // 256)
+        ntile = 128 if M <= 128 else 256  # M <= 128: 128-token pair tiles
+        pairs = (N // 256) * ((M + ntile - 1) // ntile)
         want = next((k for k in (4, 3, 2) if pairs <= SMS // (2 * k) and K // 64 >= 4 * k), 1)
         if want > 1:
-            assert (c["kind"], c["tile_m"], c["split_k"]) == (5, 256, want), c
-            assert c["grid_ctas"] == (N // 128) * want * ((M + 255) // 256)
+            assert (c["kind"], c["tile_m"], c["split_k"]) == (5, ntile, want), c
+            assert c["grid_ctas"] == (N // 128) * want * ((M + ntile - 1) // ntile)
             return
         if c["kind"] == 5:  # the tiled chooser's own unsplit 256-token tiles run on pairs
             assert c["split_k"] == 1 and c["tile_m"] == 256
